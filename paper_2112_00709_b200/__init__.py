@@ -1,0 +1,283 @@
+"""paper_2112_00709_b200 — batched log-semiring forward-backward and LF-MMI on B200.
+
+Thin Python binding over libfb.so (include/fb.h).  Each function marshals
+torch CUDA tensors to device pointers and the current CUDA stream and calls the
+C-ABI entry point of the same name; every step of the path runs in the
+library's sm_100a kernels.  There is no CPU fallback: a missing library or a
+non-CUDA tensor raises.
+
+    g = Graph.from_host(synth.compose(...))          # fb_graph_create
+    logZ, alpha, scale, st = fb_forward(g, emis, lengths)
+    post, logZb, st = fb_backward(g, emis, lengths, alpha=alpha, status=st)
+    loss, totals, st = lfmmi_loss_grad(num, den, emis, lengths, grad)
+
+Paper: arXiv 2112.00709 (PAPER.md P:173-191 log-domain recursions, P:193-227
+batching, P:266-288 LF-MMI).  See DESIGN.md.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+
+from ._lib import EXPORTS, lib  # noqa: F401
+
+__all__ = [
+    "FBError", "Graph", "fb_forward", "fb_backward", "fb_posteriors", "lfmmi_loss_grad", "workspace_bytes",
+    "fb_viterbi", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
+    "SEQ_OK", "SEQ_EMPTY_LATTICE", "SEQ_NONFINITE_INPUT", "SEQ_BAD_LENGTH",
+    "GRAPH_DEFAULT", "GRAPH_FORCE_EXACT", "GRAPH_FORCE_FACTORED",
+]
+
+SEQ_OK, SEQ_EMPTY_LATTICE, SEQ_NONFINITE_INPUT, SEQ_BAD_LENGTH = 0, 1, 2, 4
+GRAPH_DEFAULT, GRAPH_FORCE_EXACT, GRAPH_FORCE_FACTORED = 0, 1, 2
+
+
+class FBError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        L = lib()
+        msg = L.fb_status_str(code).decode()
+        if code == 4:
+            msg += f" ({L.fb_last_cuda_error().decode()})"
+        super().__init__(f"{where}: fb_status {code}: {msg}")
+        self.code = code
+
+
+def _check(code: int, where: str) -> None:
+    if code != 0:
+        raise FBError(code, where)
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dev(t, dtype, name):
+    """device pointer of a contiguous CUDA tensor of the given dtype (None → NULL)."""
+    if t is None:
+        return None
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Graph:
+    """A compiled fb_graph handle (G member graphs, block-diagonal)."""
+
+    def __init__(self, state_offsets, row_ptr, col, log_w, log_init, log_final, pdf_of, D, flags=0):
+        so = np.ascontiguousarray(state_offsets, np.int32)
+        rp = np.ascontiguousarray(row_ptr, np.int32)
+        cl = np.ascontiguousarray(col, np.int32)
+        lw = np.ascontiguousarray(log_w, np.float32)
+        li = np.ascontiguousarray(log_init, np.float32)
+        lf = np.ascontiguousarray(log_final, np.float32)
+        pd = None if pdf_of is None else np.ascontiguousarray(pdf_of, np.int32)
+        h = ctypes.c_void_p()
+        code = lib().fb_graph_create(ctypes.byref(h), len(so) - 1, _np_ptr(so), _np_ptr(rp), _np_ptr(cl),
+                                     _np_ptr(lw), _np_ptr(li), _np_ptr(lf), _np_ptr(pd), int(D), int(flags))
+        _check(code, "fb_graph_create")
+        self._h = h
+        self.G = len(so) - 1
+        self.D = int(D)
+        self.state_offsets = so
+        info = np.zeros(16, np.int64)
+        _check(lib().fb_graph_info(h, _np_ptr(info)), "fb_graph_info")
+        keys = ["G", "K_tot", "nnz", "D", "threads", "spt", "mode", "fwd_smem", "bwd_smem", "K_max", "nnz_max",
+                "fwd_slots_max", "bwd_slots_max", "U_max"]
+        self.info = {k: int(v) for k, v in zip(keys, info)}
+        self.K_tot = self.info["K_tot"]
+
+    @classmethod
+    def from_host(cls, g, flags: int = 0) -> "Graph":
+        """From a synth.HostGraph (G = 1) or synth.ComposedGraph."""
+        so = g.state_offsets if hasattr(g, "state_offsets") else np.array([0, g.K], np.int32)
+        return cls(so, g.row_ptr, g.col, g.logw, g.log_init, g.log_final, g.pdf_of, g.D, flags)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def lattice_numel(self, B: int, N_max: int) -> int:
+        return B * N_max * self.K_tot if self.G == 1 else N_max * self.K_tot
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().fb_graph_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fb_forward(g: Graph, emis, lengths, alpha=None, alpha_scale=None, want_alpha=True):
+    """Eq. (13).  Returns (logZ [B] f64, alpha, alpha_scale, status [B] i32)."""
+    import torch
+
+    B, N_max, D = emis.shape
+    dev = emis.device
+    if want_alpha and alpha is None:
+        alpha = torch.empty(g.lattice_numel(B, N_max), dtype=torch.float32, device=dev)
+    if alpha is not None and alpha_scale is None:
+        alpha_scale = torch.empty((B, N_max), dtype=torch.float64, device=dev)
+    logZ = torch.empty(B, dtype=torch.float64, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    _check(lib().fb_forward(g.handle, _dev(emis, torch.float32, "emis"), _dev(lengths, torch.int32, "lengths"),
+                            B, N_max, _dev(alpha, torch.float32, "alpha"),
+                            _dev(alpha_scale, torch.float64, "alpha_scale"), _dev(logZ, torch.float64, "logZ"),
+                            _dev(st, torch.int32, "status"), _stream()), "fb_forward")
+    return logZ, alpha, alpha_scale, st
+
+
+def fb_backward(g: Graph, emis, lengths, alpha=None, status=None, want_beta=False, post="state", post_out=None):
+    """Eq. (14) (v_{n+1}) with the fused posterior epilogue (Eq. (15)).
+
+    post: "state" (lattice layout γ), "pdf" ([B,N_max,D] Γ) or None.
+    Returns (post, logZ_beta, status, beta, beta_scale)."""
+    import torch
+
+    B, N_max, D = emis.shape
+    dev = emis.device
+    if status is None:
+        status = torch.zeros(B, dtype=torch.int32, device=dev)
+    beta = beta_scale = None
+    if want_beta:
+        beta = torch.empty(g.lattice_numel(B, N_max), dtype=torch.float32, device=dev)
+        beta_scale = torch.empty((B, N_max), dtype=torch.float64, device=dev)
+    pdf_level = 0
+    if post is not None:
+        if alpha is None:
+            raise ValueError("posteriors need the forward lattice `alpha`")
+        pdf_level = 1 if post == "pdf" else 0
+        if post_out is None:
+            post_out = torch.empty((B, N_max, D) if pdf_level else (g.lattice_numel(B, N_max),),
+                                   dtype=torch.float32, device=dev)
+    logZb = torch.empty(B, dtype=torch.float64, device=dev)
+    _check(lib().fb_backward(g.handle, _dev(emis, torch.float32, "emis"), _dev(lengths, torch.int32, "lengths"),
+                             B, N_max, _dev(beta, torch.float32, "beta"), _dev(beta_scale, torch.float64, "beta_scale"),
+                             _dev(logZb, torch.float64, "logZ_beta"), _dev(alpha, torch.float32, "alpha"),
+                             _dev(post_out, torch.float32, "post"), pdf_level, _dev(status, torch.int32, "status"),
+                             _stream()), "fb_backward")
+    return post_out, logZb, status, beta, beta_scale
+
+
+def fb_posteriors(g: Graph, alpha, beta, lengths, status, B, N_max, pdf_level=False, post=None):
+    """Standalone Eq. (15): exp(α̂ + β̂ − Z_n)."""
+    import torch
+
+    dev = alpha.device
+    if post is None:
+        post = torch.empty((B, N_max, g.D) if pdf_level else (g.lattice_numel(B, N_max),), dtype=torch.float32,
+                           device=dev)
+    _check(lib().fb_posteriors(g.handle, _dev(alpha, torch.float32, "alpha"), _dev(beta, torch.float32, "beta"),
+                               _dev(lengths, torch.int32, "lengths"), _dev(status, torch.int32, "status"), B, N_max,
+                               int(bool(pdf_level)), _dev(post, torch.float32, "post"), _stream()), "fb_posteriors")
+    return post
+
+
+def workspace_bytes(num: Graph, den: Graph, B: int, N_max: int) -> int:
+    return int(lib().fb_workspace_bytes(num.handle, den.handle, B, N_max))
+
+
+def lfmmi_loss_grad(num: Graph, den: Graph, emis, lengths, grad=None, workspace=None, loss=None, totals=None,
+                    status=None):
+    """LF-MMI loss and gradient.  Returns (loss [B] f64, totals [5] f64, status [B], grad)."""
+    import torch
+
+    B, N_max, D = emis.shape
+    dev = emis.device
+    if grad is None:
+        grad = torch.empty((B, N_max, D), dtype=torch.float32, device=dev)
+    nbytes = workspace_bytes(num, den, B, N_max)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    if loss is None:
+        loss = torch.empty(B, dtype=torch.float64, device=dev)
+    if totals is None:
+        totals = torch.empty(5, dtype=torch.float64, device=dev)
+    if status is None:
+        status = torch.empty(B, dtype=torch.int32, device=dev)
+    _check(lib().lfmmi_loss_grad(num.handle, den.handle, _dev(emis, torch.float32, "emis"),
+                                 _dev(lengths, torch.int32, "lengths"), B, N_max, _dev(grad, torch.float32, "grad"),
+                                 _dev(loss, torch.float64, "loss"), _dev(totals, torch.float64, "totals"),
+                                 _dev(status, torch.int32, "status"), _dev(workspace, torch.uint8, "workspace"),
+                                 workspace.numel(), _stream()), "lfmmi_loss_grad")
+    return loss, totals, status, grad
+
+
+def lfmmi_loss_grad_host(num: Graph, den: Graph, emis_host, lengths_host, bufs: dict):
+    """End-to-end call with HOST inputs: pinned φ and lengths are copied to the
+    device, lfmmi_loss_grad runs, and the totals (and per-utterance loss) are
+    copied back.  `bufs` caches the device buffers between calls."""
+    import torch
+
+    B, N_max, D = emis_host.shape
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if "emis" not in bufs:
+        bufs["emis"] = torch.empty((B, N_max, D), dtype=torch.float32, device=dev)
+        bufs["lengths"] = torch.empty(B, dtype=torch.int32, device=dev)
+        bufs["grad"] = torch.empty((B, N_max, D), dtype=torch.float32, device=dev)
+        bufs["ws"] = torch.empty(workspace_bytes(num, den, B, N_max), dtype=torch.uint8, device=dev)
+        bufs["loss"] = torch.empty(B, dtype=torch.float64, device=dev)
+        bufs["totals"] = torch.empty(5, dtype=torch.float64, device=dev)
+        bufs["status"] = torch.empty(B, dtype=torch.int32, device=dev)
+        bufs["out"] = torch.empty(5 + B, dtype=torch.float64).pin_memory()
+    bufs["emis"].copy_(emis_host, non_blocking=True)
+    bufs["lengths"].copy_(lengths_host, non_blocking=True)
+    lfmmi_loss_grad(num, den, bufs["emis"], bufs["lengths"], bufs["grad"], bufs["ws"], bufs["loss"], bufs["totals"],
+                    bufs["status"])
+    bufs["out"][:5].copy_(bufs["totals"], non_blocking=True)
+    bufs["out"][5:].copy_(bufs["loss"], non_blocking=True)
+    return bufs["out"]
+
+
+def fb_viterbi(g: Graph, emis, lengths):
+    """Tropical-semiring best path.  Returns (score [B] f64, path [B,N_max] i32, status)."""
+    import torch
+
+    B, N_max, D = emis.shape
+    dev = emis.device
+    nbytes = int(lib().fb_viterbi_workspace_bytes(g.handle, B, N_max))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    path = torch.empty((B, N_max), dtype=torch.int32, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    _check(lib().fb_viterbi(g.handle, _dev(emis, torch.float32, "emis"), _dev(lengths, torch.int32, "lengths"), B,
+                            N_max, _dev(score, torch.float64, "score"), _dev(path, torch.int32, "path"),
+                            _dev(st, torch.int32, "status"), _dev(ws, torch.uint8, "workspace"), ws.numel(),
+                            _stream()), "fb_viterbi")
+    return score, path, st
+
+
+def profile_enable(on: bool = True) -> None:
+    lib().fb_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    lib().fb_profile_reset()
+
+
+def profile_collect() -> dict:
+    """{kernel name: (launches, summed device ms)} since the last reset."""
+    cap = 32
+    names = (ctypes.c_char_p * cap)()
+    counts = np.zeros(cap, np.int64)
+    ms = np.zeros(cap, np.float64)
+    n = ctypes.c_int32(0)
+    _check(lib().fb_profile_collect(names, _np_ptr(counts), _np_ptr(ms), cap, ctypes.byref(n)), "fb_profile_collect")
+    return {names[i].decode(): (int(counts[i]), float(ms[i])) for i in range(n.value)}

@@ -1,0 +1,401 @@
+// fb_graph.cpp — host-side graph compiler for libfb (fb_graph_create/destroy/info).
+//
+// Turns G CSR automata (block-diagonal batch P:202-224) into what the
+// one-CTA-per-sequence kernels consume:
+//   • per direction (forward pulls over in-arcs = CSC of T, ledger L3; backward
+//     pulls over out-arcs = CSR), an nnz-balanced per-thread arc schedule: rows
+//     are split into segments of at most ⌈nnz/T⌉ arcs, segments are packed onto
+//     the T threads longest-first (LPT), and each warp's arcs are laid out
+//     slot-major so that every lane reads its record with one conflict-free
+//     64-bit shared-memory load per slot;
+//   • BFS viability distances (min #transitions to a final / from an initial
+//     state) for exact masking of states that carry no posterior mass;
+//   • the inverse state→pdf map (ledger L9) as ascending per-pdf state lists.
+// Everything is computed once here and uploaded in a single allocation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <new>
+#include <numeric>
+#include <queue>
+#include <vector>
+
+#include "fb_internal.h"
+
+namespace fbx {
+
+static const double kLog2e = 1.4426950408889634;
+static const int kFar = INT_MAX / 4;
+
+namespace {
+
+struct HostSched {
+    std::vector<uint2> rec;
+    std::vector<int> rec_rows, warp_row, warp_nslot, lane_cnt, segptr, nseg;
+    std::vector<long long> rec_off;
+    int rows_max = 0, nseg_max = 0, slots_max = 0;
+};
+
+// Arc lists for one member graph in one direction: row r reduces over
+// (other[a], w[a]) for a in [ptr[r], ptr[r+1]), ascending `other`.
+struct RowLists {
+    std::vector<int> ptr, other;
+    std::vector<double> w;  // natural log
+};
+
+// Per-thread nnz-balanced schedule for one member (appends to hs).
+bool build_member_sched(const RowLists &rl, int K, int T, int mode, HostSched &hs) {
+    const int W = T / 32;
+    const long long nnz = rl.ptr[K];
+    const long long L = std::max<long long>(1, (nnz + T - 1) / T);
+    // segments in row order
+    std::vector<int> seg_row, seg_begin, seg_len;
+    std::vector<int> segptr(K + 1, 0);
+    for (int r = 0; r < K; ++r) {
+        segptr[r] = (int)seg_row.size();
+        long long deg = rl.ptr[r + 1] - rl.ptr[r];
+        if (deg == 0) continue;
+        long long ns = (deg + L - 1) / L;
+        long long base = deg / ns, rem = deg % ns, b = rl.ptr[r];
+        for (long long s = 0; s < ns; ++s) {
+            long long len = base + (s < rem ? 1 : 0);
+            seg_row.push_back(r);
+            seg_begin.push_back((int)b);
+            seg_len.push_back((int)len);
+            b += len;
+        }
+    }
+    segptr[K] = (int)seg_row.size();
+    const int nseg = (int)seg_row.size();
+    if (nseg > 65535 || K > 65536) return false;
+    // LPT: longest segment first onto the least-loaded thread (ties → lowest id)
+    std::vector<int> order(nseg);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return seg_len[a] > seg_len[b]; });
+    using Item = std::pair<long long, int>;
+    std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
+    for (int t = 0; t < T; ++t) heap.push({0, t});
+    std::vector<std::vector<int>> tsegs(T);
+    for (int s : order) {
+        Item it = heap.top();
+        heap.pop();
+        tsegs[it.second].push_back(s);
+        heap.push({it.first + seg_len[s], it.second});
+    }
+    std::vector<int> lane_cnt(T, 0);
+    for (int t = 0; t < T; ++t) {
+        std::sort(tsegs[t].begin(), tsegs[t].end());
+        for (int s : tsegs[t]) lane_cnt[t] += seg_len[s];
+    }
+    std::vector<int> warp_row(W), warp_nslot(W);
+    int rows = 0, slots_max = 0;
+    for (int w = 0; w < W; ++w) {
+        int mx = 0;
+        for (int l = 0; l < 32; ++l) mx = std::max(mx, lane_cnt[w * 32 + l]);
+        warp_row[w] = rows;
+        warp_nslot[w] = mx;
+        rows += mx;
+        slots_max = std::max(slots_max, mx);
+    }
+    const long long off = (long long)hs.rec.size();
+    uint2 pad;
+    pad.x = 0u;
+    float padw = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
+    std::memcpy(&pad.y, &padw, 4);
+    hs.rec.resize(off + (long long)rows * 32, pad);
+    for (int t = 0; t < T; ++t) {
+        int w = t / 32, l = t % 32, slot = 0;
+        for (int s : tsegs[t]) {
+            for (int q = 0; q < seg_len[s]; ++q) {
+                int a = seg_begin[s] + q;
+                uint2 r;
+                r.x = (uint32_t)rl.other[a] & 0xFFFFu;
+                if (q == seg_len[s] - 1) r.x |= (uint32_t)(s + 1) << 16;
+                double wn = rl.w[a];
+                float wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
+                if (std::isinf(wn) && wn < 0) wf = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
+                std::memcpy(&r.y, &wf, 4);
+                hs.rec[off + ((long long)warp_row[w] + slot) * 32 + l] = r;
+                ++slot;
+            }
+        }
+    }
+    hs.rec_off.push_back(off);
+    hs.rec_rows.push_back(rows);
+    hs.warp_row.insert(hs.warp_row.end(), warp_row.begin(), warp_row.end());
+    hs.warp_nslot.insert(hs.warp_nslot.end(), warp_nslot.begin(), warp_nslot.end());
+    hs.lane_cnt.insert(hs.lane_cnt.end(), lane_cnt.begin(), lane_cnt.end());
+    hs.segptr.insert(hs.segptr.end(), segptr.begin(), segptr.end());
+    hs.nseg.push_back(nseg);
+    hs.rows_max = std::max(hs.rows_max, rows);
+    hs.nseg_max = std::max(hs.nseg_max, nseg);
+    hs.slots_max = std::max(hs.slots_max, slots_max);
+    return true;
+}
+
+int pow2ceil(long long x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct Packer {
+    std::vector<unsigned char> buf;
+    template <class T>
+    size_t put(const std::vector<T> &v) {
+        size_t off = align16(buf.size());
+        buf.resize(off + v.size() * sizeof(T) + 16);
+        if (!v.empty()) std::memcpy(buf.data() + off, v.data(), v.size() * sizeof(T));
+        return off;
+    }
+};
+
+bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
+
+}  // namespace
+
+size_t smem_bytes(const Graph &g, bool backward, bool post) {
+    const Sched &s = backward ? g.bwd : g.fwd;
+    size_t b = 0;
+    b += align16((size_t)s.rows_max * 32 * 8);                  // arc records
+    b += align16((size_t)g.K_max * 4);                          // u (log2 domain)
+    if (g.mode == MODE_FACTORED) b += align16((size_t)g.K_max * 4);  // p = exp2(u)
+    b += align16((size_t)std::max(1, s.nseg_max) * 4);          // segment partials
+    if (backward && post) b += align16((size_t)g.K_max * 4);    // γ row for the pdf gather
+    b += align16(4 * (2 * 32 + 2 * 64 + 32));                  // reductions + flags
+    return b;
+}
+
+}  // namespace fbx
+
+using namespace fbx;
+
+extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *state_offsets,
+                                     const int32_t *row_ptr, const int32_t *col, const float *log_w,
+                                     const float *log_init, const float *log_final,
+                                     const int32_t *pdf_of, int32_t D, int32_t flags) {
+    if (!out || G < 1 || !state_offsets || !row_ptr || !log_init || !log_final || D < 1)
+        return FB_ERR_INVALID_ARG;
+    if (D > (1 << 20)) return FB_ERR_UNSUPPORTED;  // pdf ids are packed in 20 bits on device
+    *out = nullptr;
+    if (state_offsets[0] != 0) return FB_ERR_INVALID_GRAPH;
+    for (int g = 0; g < G; ++g)
+        if (state_offsets[g + 1] <= state_offsets[g]) return FB_ERR_INVALID_GRAPH;
+    const int K_tot = state_offsets[G];
+    if (row_ptr[0] != 0) return FB_ERR_INVALID_GRAPH;
+    for (int i = 0; i < K_tot; ++i)
+        if (row_ptr[i + 1] < row_ptr[i]) return FB_ERR_INVALID_GRAPH;
+    const long long nnz = row_ptr[K_tot];
+    if (nnz > 0 && (!col || !log_w)) return FB_ERR_INVALID_ARG;
+
+    Graph gr;
+    gr.G = G;
+    gr.K_tot = K_tot;
+    gr.D = D;
+    gr.nnz = nnz;
+    std::vector<int> member(K_tot);
+    for (int g = 0; g < G; ++g) {
+        int K = state_offsets[g + 1] - state_offsets[g];
+        if (K > 65536) return FB_ERR_UNSUPPORTED;
+        gr.K_max = std::max(gr.K_max, K);
+        gr.nnz_max = std::max<long long>(gr.nnz_max, row_ptr[state_offsets[g + 1]] - row_ptr[state_offsets[g]]);
+        for (int k = state_offsets[g]; k < state_offsets[g + 1]; ++k) member[k] = g;
+    }
+    // validate arcs, weights, pdfs
+    bool factored_ok = true;
+    for (int i = 0; i < K_tot; ++i) {
+        int g = member[i];
+        for (int a = row_ptr[i]; a < row_ptr[i + 1]; ++a) {
+            if (col[a] < state_offsets[g] || col[a] >= state_offsets[g + 1]) return FB_ERR_INVALID_GRAPH;
+            if (bad(log_w[a])) return FB_ERR_INVALID_GRAPH;
+            if (!(std::isinf(log_w[a]) && log_w[a] < 0) && (log_w[a] < -80.0f || log_w[a] > 80.0f))
+                factored_ok = false;
+        }
+        if (bad(log_init[i]) || bad(log_final[i])) return FB_ERR_INVALID_GRAPH;
+    }
+    std::vector<int> pdf(K_tot);
+    for (int i = 0; i < K_tot; ++i) {
+        int p = pdf_of ? pdf_of[i] : i - state_offsets[member[i]];
+        if (p < 0 || p >= D) return pdf_of ? FB_ERR_INVALID_GRAPH : FB_ERR_SHAPE;
+        pdf[i] = p;
+    }
+    // ⊕ evaluation mode: exp-factorised rows pay off on large
+    // ergodic graphs; small / left-to-right graphs use max-then-sum.
+    if (flags & FB_GRAPH_FORCE_EXACT) {
+        gr.mode = MODE_EXACT;
+    } else if (flags & FB_GRAPH_FORCE_FACTORED) {
+        if (!factored_ok) return FB_ERR_UNSUPPORTED;
+        gr.mode = MODE_FACTORED;
+    } else {
+        long long nnz_min = LLONG_MAX;
+        for (int g = 0; g < G; ++g)
+            nnz_min = std::min<long long>(nnz_min, row_ptr[state_offsets[g + 1]] - row_ptr[state_offsets[g]]);
+        gr.mode = (factored_ok && nnz_min >= 4096) ? MODE_FACTORED : MODE_EXACT;
+    }
+    // threads per CTA and states per thread
+    int T = gr.nnz_max >= 16384 ? 1024 : std::min(1024, std::max(32, pow2ceil((gr.nnz_max + 15) / 16)));
+    T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
+    T = std::max(T, 32);
+    int spt = pow2ceil((gr.K_max + T - 1) / T);
+    if (spt > kMaxSPT) return FB_ERR_UNSUPPORTED;
+    gr.T = T;
+    gr.W = T / 32;
+    gr.spt = spt;
+
+    // per-member schedules, distances, pdf slots
+    HostSched hf, hb;
+    std::vector<int> dist_fin(K_tot, kFar), dist_start(K_tot, kFar);
+    std::vector<int> slot_off(G + 1, 0), slot_pdf, slot_sptr(1, 0), slot_states;
+    std::vector<int> pdf_slot((size_t)G * D, -1);
+    std::vector<float> init2(K_tot), final2(K_tot);
+    for (int i = 0; i < K_tot; ++i) {
+        init2[i] = (float)((double)log_init[i] * kLog2e);
+        final2[i] = (float)((double)log_final[i] * kLog2e);
+    }
+    for (int g = 0; g < G; ++g) {
+        const int s0 = state_offsets[g], K = state_offsets[g + 1] - s0;
+        RowLists in, outl;
+        in.ptr.assign(K + 1, 0);
+        outl.ptr.assign(K + 1, 0);
+        // out-arcs (CSR), sorted by destination within a row (stable for duplicates)
+        std::vector<std::pair<int, int>> tmp;
+        for (int i = 0; i < K; ++i) {
+            tmp.clear();
+            for (int a = row_ptr[s0 + i]; a < row_ptr[s0 + i + 1]; ++a) tmp.push_back({col[a] - s0, a});
+            std::stable_sort(tmp.begin(), tmp.end(), [](auto &x, auto &y) { return x.first < y.first; });
+            for (auto &pr : tmp) {
+                outl.other.push_back(pr.first);
+                outl.w.push_back(log_w[pr.second]);
+                in.ptr[pr.first + 1]++;
+            }
+            outl.ptr[i + 1] = (int)outl.other.size();
+        }
+        // in-arcs (CSC) in ascending source order
+        for (int j = 0; j < K; ++j) in.ptr[j + 1] += in.ptr[j];
+        in.other.resize(outl.other.size());
+        in.w.resize(outl.other.size());
+        std::vector<int> fill(K, 0);
+        for (int i = 0; i < K; ++i)
+            for (int a = outl.ptr[i]; a < outl.ptr[i + 1]; ++a) {
+                int j = outl.other[a];
+                int p = in.ptr[j] + fill[j]++;
+                in.other[p] = i;
+                in.w[p] = outl.w[a];
+            }
+        if (!build_member_sched(in, K, T, gr.mode, hf)) return FB_ERR_UNSUPPORTED;
+        if (!build_member_sched(outl, K, T, gr.mode, hb)) return FB_ERR_UNSUPPORTED;
+        // BFS over finite arcs: distance to a final state (reverse) / from an initial state
+        std::deque<int> q;
+        for (int k = 0; k < K; ++k)
+            if (!(std::isinf(log_final[s0 + k]) && log_final[s0 + k] < 0)) { dist_fin[s0 + k] = 0; q.push_back(k); }
+        while (!q.empty()) {
+            int j = q.front(); q.pop_front();
+            for (int a = in.ptr[j]; a < in.ptr[j + 1]; ++a) {
+                if (std::isinf(in.w[a]) && in.w[a] < 0) continue;
+                int i = in.other[a];
+                if (dist_fin[s0 + i] == kFar) { dist_fin[s0 + i] = dist_fin[s0 + j] + 1; q.push_back(i); }
+            }
+        }
+        for (int k = 0; k < K; ++k)
+            if (!(std::isinf(log_init[s0 + k]) && log_init[s0 + k] < 0)) { dist_start[s0 + k] = 0; q.push_back(k); }
+        while (!q.empty()) {
+            int i = q.front(); q.pop_front();
+            for (int a = outl.ptr[i]; a < outl.ptr[i + 1]; ++a) {
+                if (std::isinf(outl.w[a]) && outl.w[a] < 0) continue;
+                int j = outl.other[a];
+                if (dist_start[s0 + j] == kFar) { dist_start[s0 + j] = dist_start[s0 + i] + 1; q.push_back(j); }
+            }
+        }
+        // inverse pdf map: distinct pdfs ascending, states ascending
+        std::vector<std::pair<int, int>> ps;
+        for (int k = 0; k < K; ++k) ps.push_back({pdf[s0 + k], k});
+        std::sort(ps.begin(), ps.end());
+        int local = 0;
+        for (size_t x = 0; x < ps.size(); ++x) {
+            if (x == 0 || ps[x].first != ps[x - 1].first) {
+                if (x) slot_sptr.push_back((int)slot_states.size());
+                slot_pdf.push_back(ps[x].first);
+                pdf_slot[(size_t)g * D + ps[x].first] = local++;
+            }
+            slot_states.push_back(ps[x].second);
+        }
+        slot_sptr.push_back((int)slot_states.size());
+        slot_off[g + 1] = slot_off[g] + local;
+        gr.pm.U_max = std::max(gr.pm.U_max, local);
+    }
+    gr.pm.U_tot = slot_off[G];
+    gr.fwd.rows_max = hf.rows_max; gr.fwd.nseg_max = hf.nseg_max; gr.fwd.slots_max = hf.slots_max;
+    gr.bwd.rows_max = hb.rows_max; gr.bwd.nseg_max = hb.nseg_max; gr.bwd.slots_max = hb.slots_max;
+    if (smem_bytes(gr, false, false) > (size_t)kSmemLimit || smem_bytes(gr, true, true) > (size_t)kSmemLimit)
+        return FB_ERR_UNSUPPORTED;
+
+    // pack and upload
+    Packer pk;
+    std::vector<int> soff(state_offsets, state_offsets + G + 1);
+    size_t o_soff = pk.put(soff), o_pdf = pk.put(pdf), o_i2 = pk.put(init2), o_f2 = pk.put(final2);
+    size_t o_df = pk.put(dist_fin), o_ds = pk.put(dist_start);
+    size_t o_frec = pk.put(hf.rec), o_frr = pk.put(hf.rec_rows), o_fro = pk.put(hf.rec_off),
+           o_fwr = pk.put(hf.warp_row), o_fwn = pk.put(hf.warp_nslot), o_flc = pk.put(hf.lane_cnt),
+           o_fsp = pk.put(hf.segptr), o_fns = pk.put(hf.nseg);
+    size_t o_brec = pk.put(hb.rec), o_brr = pk.put(hb.rec_rows), o_bro = pk.put(hb.rec_off),
+           o_bwr = pk.put(hb.warp_row), o_bwn = pk.put(hb.warp_nslot), o_blc = pk.put(hb.lane_cnt),
+           o_bsp = pk.put(hb.segptr), o_bns = pk.put(hb.nseg);
+    size_t o_so = pk.put(slot_off), o_spd = pk.put(slot_pdf), o_ssp = pk.put(slot_sptr),
+           o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot);
+    void *dev = nullptr;
+    cudaGetDevice(&gr.device);
+    cudaError_t e = cudaMalloc(&dev, pk.buf.size());
+    if (e != cudaSuccess) { set_cuda_error("cudaMalloc(graph)", (int)e); return FB_ERR_NOMEM; }
+    e = cudaMemcpy(dev, pk.buf.data(), pk.buf.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(dev); set_cuda_error("cudaMemcpy(graph)", (int)e); return FB_ERR_CUDA; }
+    auto P = [&](size_t off) { return (const void *)((const unsigned char *)dev + off); };
+    gr.block = dev;
+    gr.block_bytes = pk.buf.size();
+    gr.state_off = (const int *)P(o_soff);
+    gr.pdf = (const int *)P(o_pdf);
+    gr.init2 = (const float *)P(o_i2);
+    gr.final2 = (const float *)P(o_f2);
+    gr.dist_fin = (const int *)P(o_df);
+    gr.dist_start = (const int *)P(o_ds);
+    gr.fwd.rec = (const uint2 *)P(o_frec); gr.fwd.rec_rows = (const int *)P(o_frr);
+    gr.fwd.rec_off = (const long long *)P(o_fro); gr.fwd.warp_row = (const int *)P(o_fwr);
+    gr.fwd.warp_nslot = (const int *)P(o_fwn); gr.fwd.lane_cnt = (const int *)P(o_flc);
+    gr.fwd.segptr = (const int *)P(o_fsp); gr.fwd.nseg = (const int *)P(o_fns);
+    gr.bwd.rec = (const uint2 *)P(o_brec); gr.bwd.rec_rows = (const int *)P(o_brr);
+    gr.bwd.rec_off = (const long long *)P(o_bro); gr.bwd.warp_row = (const int *)P(o_bwr);
+    gr.bwd.warp_nslot = (const int *)P(o_bwn); gr.bwd.lane_cnt = (const int *)P(o_blc);
+    gr.bwd.segptr = (const int *)P(o_bsp); gr.bwd.nseg = (const int *)P(o_bns);
+    gr.pm.slot_off = (const int *)P(o_so); gr.pm.slot_pdf = (const int *)P(o_spd);
+    gr.pm.slot_sptr = (const int *)P(o_ssp); gr.pm.slot_states = (const int *)P(o_sst);
+    gr.pm.pdf_slot = (const int *)P(o_pds);
+    fb_graph h = new (std::nothrow) fb_graph_s;
+    if (!h) { cudaFree(dev); return FB_ERR_NOMEM; }
+    h->g = gr;
+    *out = h;
+    return FB_OK;
+}
+
+extern "C" fb_status fb_graph_destroy(fb_graph g) {
+    if (!g) return FB_OK;
+    cudaDeviceSynchronize();
+    cudaFree(g->g.block);
+    delete g;
+    return FB_OK;
+}
+
+extern "C" fb_status fb_graph_info(fb_graph h, int64_t *out) {
+    if (!h || !out) return FB_ERR_INVALID_ARG;
+    const Graph &g = h->g;
+    int64_t v[16] = {g.G, g.K_tot, g.nnz, g.D, g.T, g.spt, g.mode,
+                     (int64_t)smem_bytes(g, false, false), (int64_t)smem_bytes(g, true, true),
+                     g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max, 0, 0};
+    std::memcpy(out, v, sizeof v);
+    return FB_OK;
+}

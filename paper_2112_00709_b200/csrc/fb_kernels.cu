@@ -1,0 +1,967 @@
+// fb_kernels.cu — sm_100a kernels and C-ABI entry points of libfb.
+//
+// One CTA per sequence runs the whole time recursion of one direction with the
+// sequence's graph schedule resident in shared memory (P:173-191 in the log
+// semifield, P:193-227 batched).  Per frame n one CTA does:
+//
+//   phase A  every lane walks its slot column of the nnz-balanced schedule and
+//            reduces its row segments: factored mode  Σ p_src·e^{T} with
+//            p = 2^{u} (one FMA per arc, exact max-then-sum fallback when the
+//            sum leaves [2^-80, 2^120]); exact mode online max-then-sum (one
+//            ex2 per arc).  Segment results (log2) go to smem `part`.
+//   barrier
+//   phase B1 per owned state: combine its segments, add the emission
+//            (forward: v_n after the product, Eq. (13); backward: v_n on the
+//            new β̂_n, Eq. (14) with ledger L2), apply the exact viability mask,
+//            warp max of the new vector.
+//   barrier
+//   phase B2 normalise by the block max (exact, so the largest viable entry is
+//            0 — SURVEY §8(c4)), accumulate the float64 scale, write α̂/β̂ to
+//            HBM, refresh u (log2) and p = 2^{u} in smem; backward also forms
+//            x = α̂_n + β̂_n and its warp log-sum-exp for the fused posterior
+//            epilogue, which is completed one frame later (no extra barrier).
+//   barrier
+//
+// All log quantities are carried in base 2 inside the kernels (ex2/lg2 are the
+// native MUFU ops) and converted to natural logs at the HBM boundary.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fb_internal.h"
+
+namespace fbx {
+
+static const float kL2E = 1.4426950408889634f;
+static const double kLN2 = 0.6931471805599453;
+
+// ------------------------------------------------------------------ error / profiling
+
+static std::mutex g_err_mu;
+static std::string g_err = "";
+
+void set_cuda_error(const char *what, int code) {
+    std::lock_guard<std::mutex> lk(g_err_mu);
+    g_err = std::string(what) + ": " + cudaGetErrorString((cudaError_t)code);
+}
+
+struct ProfRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t pool_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ProfScope {
+    bool on;
+    ProfRec r;
+    cudaStream_t s;
+    ProfScope(const char *name, cudaStream_t st) : on(false), s(st) {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        if (!g_prof_on) return;
+        on = true;
+        r.name = name;
+        r.a = pool_event();
+        r.b = pool_event();
+        cudaEventRecord(r.a, s);
+    }
+    ~ProfScope() {
+        if (!on) return;
+        cudaEventRecord(r.b, s);
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_prof.push_back(r);
+    }
+};
+
+// ------------------------------------------------------------------ device helpers
+
+#define NEG_INF (-__int_as_float(0x7f800000))
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+// (m, s) log-sum-exp pair combine: value = m + log2(s)
+__device__ __forceinline__ void lse_combine(float &m, float &s, float m2, float s2) {
+    float M = fmaxf(m, m2);
+    if (M == NEG_INF) { m = NEG_INF; s = 0.f; return; }
+    s = (m == NEG_INF ? 0.f : s * ex2(m - M)) + (m2 == NEG_INF ? 0.f : s2 * ex2(m2 - M));
+    m = M;
+}
+__device__ __forceinline__ void warp_lse(float &m, float &s) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        lse_combine(m, s, m2, s2);
+    }
+}
+__device__ __forceinline__ size_t align16d(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Online max-then-sum over one segment, re-reading its records (fallback path
+// of factored mode; weights stored as e^{T} there).
+__device__ __noinline__ float exact_segment(const uint2 *col, int s_begin, int s_end, const float *u,
+                                            bool factored) {
+    float m = NEG_INF, sum = 0.f;
+    for (int s = s_begin; s <= s_end; ++s) {
+        uint2 r = col[s * 32];
+        float w = __uint_as_float(r.y);
+        if (factored) w = log2f(w);
+        float x = u[r.x & 0xFFFFu] + w;
+        if (x == NEG_INF) continue;
+        if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
+        else sum += exp2f(x - m);
+    }
+    return m == NEG_INF ? NEG_INF : m + log2f(sum);
+}
+
+// Output kinds of the backward posterior epilogue.
+enum PostKind : int { POST_NONE = 0, POST_STATE = 1, POST_PDF_DENSE = 2, POST_PDF_COMPACT = 3, POST_GRAD = 4 };
+
+struct FBArgs {
+    Graph g;
+    const float *emis;
+    const int *lengths;
+    int B, N_max, D;
+    float *lat;         // α̂ (fwd) / β̂ (bwd) out, may be null
+    double *scale;      // [B][N_max] out, may be null
+    double *logZ;       // fwd: logZ; bwd: logZ_beta (may be null)
+    int *status;        // fwd: out; bwd: in/out
+    const int *status2; // bwd (lfmmi): numerator status, OR-ed in (may be null)
+    // backward epilogue
+    const float *alpha; // α̂ from the forward (natural log), may be null
+    int post_kind;
+    float *post;        // state / dense pdf / compact pdf / grad
+    // lfmmi gradient (POST_GRAD): Γ_num compact and the numerator pdf map
+    const float *gnum;
+    const int *num_slot_off;
+    const int *num_pdf_slot; // [B*D]
+};
+
+struct Smem {
+    uint2 *rec;
+    float *u, *p, *part, *gbuf, *wmax, *wz;
+    int *flag;
+};
+
+__device__ __forceinline__ Smem carve(unsigned char *base, const Graph &G, bool bwd, bool post, int mode) {
+    const Sched &S = bwd ? G.bwd : G.fwd;
+    Smem m;
+    size_t off = 0;
+    m.rec = (uint2 *)(base + off); off += align16d((size_t)S.rows_max * 32 * 8);
+    m.u = (float *)(base + off); off += align16d((size_t)G.K_max * 4);
+    m.p = nullptr;
+    if (mode == MODE_FACTORED) { m.p = (float *)(base + off); off += align16d((size_t)G.K_max * 4); }
+    m.part = (float *)(base + off); off += align16d((size_t)max(1, S.nseg_max) * 4);
+    m.gbuf = nullptr;
+    if (bwd && post) { m.gbuf = (float *)(base + off); off += align16d((size_t)G.K_max * 4); }
+    m.wmax = (float *)(base + off);
+    m.wz = m.wmax + 64;
+    m.flag = (int *)(m.wz + 128);
+    return m;
+}
+
+// Block-wide max of per-warp maxima stored in w[0..W-1] (every warp computes it).
+__device__ __forceinline__ float block_max_from(const float *w, int W, int lane) {
+    float v = lane < W ? w[lane] : NEG_INF;
+    return warp_max(v);
+}
+__device__ __forceinline__ float block_lse_from(const float *wz, int W, int lane) {
+    float m = lane < W ? wz[2 * lane] : NEG_INF;
+    float s = lane < W ? wz[2 * lane + 1] : 0.f;
+    warp_lse(m, s);
+    return m == NEG_INF ? NEG_INF : m + lg2(s);
+}
+
+// Combine the log2 partials of one state's segments.
+__device__ __forceinline__ float combine_segments(const float *part, int packed) {
+    int seg0 = packed & 0xFFFF, ns = packed >> 16;
+    if (ns == 0) return NEG_INF;
+    float y = part[seg0];
+    if (ns == 1) return y;
+    float m = y;
+    for (int q = 1; q < ns; ++q) m = fmaxf(m, part[seg0 + q]);
+    if (m == NEG_INF) return NEG_INF;
+    float s = 0.f;
+    for (int q = 0; q < ns; ++q) s += ex2(part[seg0 + q] - m);
+    return m + lg2(s);
+}
+
+// Phase A: reduce this lane's slot column into the segment partials.
+template <int MODE>
+__device__ __forceinline__ void phase_a(const uint2 *col, int cnt, const float *u, const float *p, float *part) {
+    constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
+    constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
+    int seg_start = 0;
+    if (MODE == MODE_FACTORED) {
+        float acc = 0.f;
+        for (int s = 0; s < cnt; s += 4) {
+            uint2 r[4];
+            float pv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r[q] = (s + q < cnt) ? col[(s + q) * 32] : make_uint2(0u, 0u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) pv[q] = p[r[q].x & 0xFFFFu];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (s + q < cnt) {
+                    acc = fmaf(pv[q], __uint_as_float(r[q].y), acc);
+                    unsigned sg = r[q].x >> 16;
+                    if (sg) {
+                        float val = (acc >= kTiny && acc <= kHuge) ? lg2(acc)
+                                                                   : exact_segment(col, seg_start, s + q, u, true);
+                        part[sg - 1] = val;
+                        acc = 0.f;
+                        seg_start = s + q + 1;
+                    }
+                }
+            }
+        }
+    } else {
+        float m = NEG_INF, sum = 0.f;
+        for (int s = 0; s < cnt; s += 4) {
+            uint2 r[4];
+            float uv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) r[q] = (s + q < cnt) ? col[(s + q) * 32] : make_uint2(0u, 0u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) uv[q] = u[r[q].x & 0xFFFFu];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (s + q < cnt) {
+                    float x = uv[q] + __uint_as_float(r[q].y);
+                    float hi = fmaxf(m, x), lo = fminf(m, x);
+                    float e = (lo == NEG_INF) ? 0.f : ex2(lo - hi);
+                    sum = (x > m) ? fmaf(sum, e, 1.f) : sum + e;
+                    m = hi;
+                    unsigned sg = r[q].x >> 16;
+                    if (sg) {
+                        part[sg - 1] = (m == NEG_INF) ? NEG_INF : m + lg2(sum);
+                        m = NEG_INF;
+                        sum = 0.f;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Write one frame's pdf-level posterior (or gradient) row from gbuf.
+__device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, int gi, int b, int n, int tid, int T) {
+    const Graph &G = a.g;
+    const PdfMap &pm = G.pm;
+    const int D = a.D;
+    if (a.post_kind == POST_PDF_COMPACT) {
+        const int so = pm.slot_off[gi], U = pm.slot_off[gi + 1] - so;
+        float *row = a.post + (size_t)a.N_max * so + (size_t)n * U;
+        for (int sl = tid; sl < U; sl += T) {
+            float acc = 0.f;
+            for (int q = pm.slot_sptr[so + sl]; q < pm.slot_sptr[so + sl + 1]; ++q) acc += gbuf[pm.slot_states[q]];
+            row[sl] = acc;
+        }
+        return;
+    }
+    const int so = pm.slot_off[gi];
+    float *row = a.post + ((size_t)b * a.N_max + n) * D;
+    const int *ps = pm.pdf_slot + (size_t)gi * D;
+    const float *gn = nullptr;
+    const int *nps = nullptr;
+    int nU = 0;
+    if (a.post_kind == POST_GRAD) {
+        const int nso = a.num_slot_off[b];
+        nU = a.num_slot_off[b + 1] - nso;
+        gn = a.gnum + (size_t)a.N_max * nso + (size_t)n * nU;
+        nps = a.num_pdf_slot + (size_t)b * D;
+    }
+    for (int d = tid; d < D; d += T) {
+        int sl = __ldg(ps + d);
+        float acc = 0.f;
+        if (sl >= 0)
+            for (int q = pm.slot_sptr[so + sl]; q < pm.slot_sptr[so + sl + 1]; ++q) acc += gbuf[pm.slot_states[q]];
+        if (a.post_kind == POST_GRAD) {
+            int ns = __ldg(nps + d);
+            float g = ns >= 0 ? gn[ns] : 0.f;
+            row[d] = g - acc;
+        } else {
+            row[d] = acc;
+        }
+    }
+}
+
+// Zero (posterior) / −∞ (lattice) rows for frames [n0, n1).
+__device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, int n0, int n1, int tid, int T,
+                               bool lattice, bool bwd) {
+    const Graph &G = a.g;
+    const size_t lat_base = (size_t)a.N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
+    for (int n = n0; n < n1; ++n) {
+        if (lattice && a.lat)
+            for (int j = tid; j < K; j += T) a.lat[lat_base + (size_t)n * K + j] = NEG_INF;
+        if (lattice && a.scale && tid == 0) a.scale[(size_t)b * a.N_max + n] = 0.0;
+        if (!bwd || a.post_kind == POST_NONE) continue;
+        if (a.post_kind == POST_STATE) {
+            for (int j = tid; j < K; j += T) a.post[lat_base + (size_t)n * K + j] = 0.f;
+        } else if (a.post_kind == POST_PDF_COMPACT) {
+            const int so = G.pm.slot_off[gi], U = G.pm.slot_off[gi + 1] - so;
+            for (int j = tid; j < U; j += T) a.post[(size_t)a.N_max * so + (size_t)n * U + j] = 0.f;
+        } else {
+            for (int d = tid; d < a.D; d += T) a.post[((size_t)b * a.N_max + n) * a.D + d] = 0.f;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ forward / backward kernel
+
+template <bool BWD, int MODE, int SPT>
+__global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Graph &G = a.g;
+    const int b = blockIdx.x;
+    const int gi = (G.G == 1) ? 0 : b;
+    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
+    const int s0 = G.state_off[gi];
+    const int K = G.state_off[gi + 1] - s0;
+    const int N = a.lengths[b];
+    const Sched &S = BWD ? G.bwd : G.fwd;
+    const bool want_post = BWD && a.post_kind != POST_NONE;
+    const bool pdf_post = want_post && a.post_kind != POST_STATE;
+    Smem sm = carve(smem_raw, G, BWD, want_post, MODE);
+
+    int st = 0;
+    if (BWD) {
+        st = a.status[b];
+        if (a.status2) st |= a.status2[b];
+    }
+    if (N < 1 || N > a.N_max) st |= FB_SEQ_BAD_LENGTH;
+    // Frames past the end (and whole flagged sequences in the backward) are written up front.
+    const bool skip = (st & FB_SEQ_BAD_LENGTH) || (BWD && st != 0);
+    write_pad_rows(a, gi, b, K, s0, skip ? 0 : N, a.N_max, tid, T, !(st & FB_SEQ_BAD_LENGTH), BWD);
+    if (skip) {
+        if (tid == 0) {
+            if (a.logZ) a.logZ[b] = -INFINITY;
+            a.status[b] = st;
+        }
+        return;
+    }
+
+    // schedule → shared memory (16-byte vector copy)
+    {
+        const uint4 *src = (const uint4 *)(S.rec + S.rec_off[gi]);
+        uint4 *dst = (uint4 *)sm.rec;
+        const int n16 = S.rec_rows[gi] * 16;
+        for (int x = tid; x < n16; x += T) dst[x] = src[x];
+    }
+    if (tid == 0) sm.flag[0] = 0;
+    const int wrow = S.warp_row[gi * W + warp];
+    const int mycnt = S.lane_cnt[gi * T + tid];
+    const uint2 *mycol = sm.rec + (size_t)wrow * 32 + lane;
+
+    // owned states j = tid + k*T: packed segment range, pdf | viability distance
+    int segp[SPT];
+    unsigned pdfd[SPT];
+    const int *segptr = S.segptr + s0 + gi;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+        int j = tid + k * T;
+        if (j < K) {
+            int a0 = segptr[j], a1 = segptr[j + 1];
+            segp[k] = a0 | ((a1 - a0) << 16);
+            int dist = BWD ? G.dist_start[s0 + j] : G.dist_fin[s0 + j];
+            dist = min(dist, 4095);
+            pdfd[k] = (unsigned)G.pdf[s0 + j] | ((unsigned)dist << 20);
+        } else {
+            segp[k] = 0;
+            pdfd[k] = 4095u << 20;
+        }
+    }
+    const float *em = a.emis + (size_t)b * a.N_max * a.D;
+    const size_t lat_base = (size_t)a.N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
+    auto load_v = [&](int n, float *v) {
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            int j = tid + k * T;
+            v[k] = (j < K && n >= 0 && n < N) ? __ldg(em + (size_t)n * a.D + (pdfd[k] & 0xFFFFF)) : 0.f;
+        }
+    };
+    auto load_alpha = [&](int n, float *v) {
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            int j = tid + k * T;
+            v[k] = (j < K && n >= 0 && n < N) ? __ldg(a.alpha + lat_base + (size_t)n * K + j) : 0.f;
+        }
+    };
+    // viable(j, n): forward — a final state is reachable in the N-1-n remaining
+    // transitions; backward — the state is reachable from an initial state in n.
+    auto viable = [&](int k, int n) {
+        int dist = (int)(pdfd[k] >> 20);
+        return BWD ? (dist <= n) : (dist <= N - 1 - n);
+    };
+
+    float vcur[SPT], vnxt[SPT];   // emissions of the frame being produced and the next one
+    float acur[SPT], anxt[SPT];   // α̂ prefetch (backward epilogue)
+    float cand[SPT], ucand[SPT];  // new α̂ / β̂ candidates and (bwd) v + β̂
+    float xpost[SPT];             // α̂_n + β̂_n of the frame whose posterior is pending
+    const int dir = BWD ? -1 : 1;
+    const int n_first = BWD ? N - 1 : 0;
+    load_v(n_first, vcur);
+    load_v(n_first + dir, vnxt);
+    if (want_post) { load_alpha(n_first, acur); load_alpha(n_first + dir, anxt); }
+    double scale = 0.0;   // C_n (fwd) / D_n (bwd), log2 units
+    bool bad = false;
+    bool pend = false;    // a posterior row is pending (its Z in wz[parity])
+    int pend_n = 0;
+    __syncthreads();  // schedule, flag visible
+
+    // ---- frame n_first: π ⊗ v_0 (fwd, L6) / β̂_{N-1} = ω (bwd, L7)
+    {
+        float lmax = NEG_INF;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            int j = tid + k * T;
+            if (j >= K) { cand[k] = NEG_INF; ucand[k] = NEG_INF; continue; }
+            float v = vcur[k];
+            if (!(v < INFINITY)) bad = true;
+            float v2 = v * kL2E;
+            if (!BWD) {
+                cand[k] = viable(k, 0) ? G.init2[s0 + j] + v2 : NEG_INF;
+                lmax = fmaxf(lmax, cand[k]);
+            } else {
+                cand[k] = viable(k, N - 1) ? G.final2[s0 + j] : NEG_INF;
+                ucand[k] = cand[k] + v2;
+                lmax = fmaxf(lmax, ucand[k]);
+            }
+        }
+        lmax = warp_max(lmax);
+        if (lane == 0) sm.wmax[warp] = lmax;
+    }
+    __syncthreads();
+    int n = n_first;
+    for (int step = 0;; ++step) {
+        // ---- phase B2 of frame n: normalise, store, refresh u/p
+        {
+            float c = block_max_from(sm.wmax + (step & 1) * 32, W, lane);
+            if (c == NEG_INF) c = 0.f;  // no viable state: keep 0̄ everywhere
+            scale += (double)c;
+            if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
+            float zm = NEG_INF, zs = 0.f;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                int j = tid + k * T;
+                if (j >= K) continue;
+                float h = cand[k] - c;   // α̂_n or β̂_n (log2)
+                float uu = BWD ? ucand[k] - c : h;
+                if (a.lat) a.lat[lat_base + (size_t)n * K + j] = h * (float)kLN2;
+                sm.u[j] = uu;
+                if (MODE == MODE_FACTORED) sm.p[j] = ex2(uu);
+                ucand[k] = uu;
+                if (want_post) {
+                    float x = acur[k] * kL2E + h;
+                    xpost[k] = x;
+                    if (x > zm) { zs = (zm == NEG_INF ? 0.f : zs * ex2(zm - x)) + 1.f; zm = x; }
+                    else if (x != NEG_INF) zs += ex2(x - zm);
+                }
+            }
+            if (want_post) {
+                warp_lse(zm, zs);
+                if (lane == 0) { sm.wz[(step & 1) * 64 + 2 * warp] = zm; sm.wz[(step & 1) * 64 + 2 * warp + 1] = zs; }
+            }
+        }
+        const int n_next = n + dir;
+        const bool last = BWD ? (n_next < 0) : (n_next >= N);
+        __syncthreads();
+        if (last) {
+            if (want_post) { pend = true; pend_n = n; }
+            break;
+        }
+        if (want_post) { pend = true; pend_n = n; }
+        // rotate prefetch: frame n_next becomes current, issue n_next + dir
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) { vcur[k] = vnxt[k]; }
+        load_v(n_next + dir, vnxt);
+        if (want_post) {
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) acur[k] = anxt[k];
+            load_alpha(n_next + dir, anxt);
+        }
+        n = n_next;
+        // ---- phase A of frame n
+        phase_a<MODE>(mycol, mycnt, sm.u, sm.p, sm.part);
+        __syncthreads();
+        // ---- phase B1 of frame n (+ pending posterior of frame n - dir)
+        {
+            if (pend) {
+                float Z = block_lse_from(sm.wz + ((step) & 1) * 64, W, lane);
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) {
+                    int j = tid + k * T;
+                    if (j >= K) continue;
+                    float gam = (Z == NEG_INF) ? 0.f : ex2(xpost[k] - Z);
+                    if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pend_n * K + j] = gam;
+                    else sm.gbuf[j] = gam;
+                }
+            }
+            float lmax = NEG_INF;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                int j = tid + k * T;
+                if (j >= K) { cand[k] = NEG_INF; ucand[k] = NEG_INF; continue; }
+                float y = combine_segments(sm.part, segp[k]);
+                float v = vcur[k];
+                if (!(v < INFINITY)) bad = true;
+                float v2 = v * kL2E;
+                bool ok = viable(k, n);
+                if (!BWD) {
+                    cand[k] = ok ? y + v2 : NEG_INF;
+                    lmax = fmaxf(lmax, cand[k]);
+                } else {
+                    cand[k] = ok ? y : NEG_INF;
+                    ucand[k] = cand[k] + v2;
+                    lmax = fmaxf(lmax, ucand[k]);
+                }
+            }
+            lmax = warp_max(lmax);
+            if (lane == 0) sm.wmax[((step + 1) & 1) * 32 + warp] = lmax;
+        }
+        __syncthreads();
+        if (pdf_post && pend) pdf_row(a, sm.gbuf, gi, b, pend_n, tid, T);
+        pend = false;
+    }
+    // ---- flush the last pending posterior row (frame 0 in the backward).  The
+    // loop ran N B2 phases (steps 0..N-1), so its wz parity is (N-1) & 1.
+    const int lastpar = (N - 1) & 1;
+    if (want_post && pend) {
+        float Z = block_lse_from(sm.wz + lastpar * 64, W, lane);
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            int j = tid + k * T;
+            if (j >= K) continue;
+            float gam = (Z == NEG_INF) ? 0.f : ex2(xpost[k] - Z);
+            if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pend_n * K + j] = gam;
+            else sm.gbuf[j] = gam;
+        }
+        __syncthreads();
+        if (pdf_post) pdf_row(a, sm.gbuf, gi, b, pend_n, tid, T);
+    }
+    // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
+    {
+        float zm = NEG_INF, zs = 0.f;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            int j = tid + k * T;
+            if (j >= K) continue;
+            float x = ucand[k] + (BWD ? G.init2[s0 + j] : G.final2[s0 + j]);
+            if (x > zm) { zs = (zm == NEG_INF ? 0.f : zs * ex2(zm - x)) + 1.f; zm = x; }
+            else if (x != NEG_INF) zs += ex2(x - zm);
+        }
+        if (bad) sm.flag[0] = 1;
+        warp_lse(zm, zs);
+        __syncthreads();  // all readers of wz[lastpar] are done
+        if (lane == 0) { sm.wz[(lastpar ^ 1) * 64 + 2 * warp] = zm; sm.wz[(lastpar ^ 1) * 64 + 2 * warp + 1] = zs; }
+        __syncthreads();
+        if (warp == 0) {
+            float m = lane < W ? sm.wz[(lastpar ^ 1) * 64 + 2 * lane] : NEG_INF;
+            float s = lane < W ? sm.wz[(lastpar ^ 1) * 64 + 2 * lane + 1] : 0.f;
+            warp_lse(m, s);
+            if (lane == 0) {
+                double z = (m == NEG_INF) ? -INFINITY : (scale + (double)m + (double)log2f(s)) * kLN2;
+                int stt = st;
+                if (sm.flag[0]) stt |= FB_SEQ_NONFINITE_INPUT;
+                if (!(z > -INFINITY)) stt |= FB_SEQ_EMPTY_LATTICE;
+                if (stt) z = -INFINITY;
+                if (a.logZ) a.logZ[b] = z;
+                a.status[b] = stt;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ standalone posteriors
+
+// One CTA per (b, n) row: Z_n = ⊕_k α̂ + β̂, γ = exp(α̂ + β̂ − Z_n) (Eq. (15)).
+__global__ void __launch_bounds__(256) k_posteriors(const Graph G, const float *alpha, const float *beta,
+                                                    const int *lengths, const int *status, int B, int N_max,
+                                                    int D, int pdf_level, float *post) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float *g = (float *)smem_raw;  // K_max
+    __shared__ float wz[2 * 32];
+    const int row = blockIdx.x;
+    const int b = row / N_max, n = row % N_max;
+    const int gi = (G.G == 1) ? 0 : b;
+    const int s0 = G.state_off[gi], K = G.state_off[gi + 1] - s0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
+    const int N = lengths[b];
+    const bool zero = (N < 1 || N > N_max || n >= N || (status && status[b] != 0));
+    const size_t base = (size_t)N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0) + (size_t)n * K;
+    if (zero) {
+        if (pdf_level) for (int d = tid; d < D; d += blockDim.x) post[((size_t)b * N_max + n) * D + d] = 0.f;
+        else for (int j = tid; j < K; j += blockDim.x) post[base + j] = 0.f;
+        return;
+    }
+    float zm = NEG_INF, zs = 0.f;
+    for (int j = tid; j < K; j += blockDim.x) {
+        float x = (__ldg(alpha + base + j) + __ldg(beta + base + j)) * kL2E;
+        g[j] = x;
+        if (x > zm) { zs = (zm == NEG_INF ? 0.f : zs * ex2(zm - x)) + 1.f; zm = x; }
+        else if (x != NEG_INF) zs += ex2(x - zm);
+    }
+    warp_lse(zm, zs);
+    if (lane == 0) { wz[2 * warp] = zm; wz[2 * warp + 1] = zs; }
+    __syncthreads();
+    float Z = block_lse_from(wz, W, lane);
+    for (int j = tid; j < K; j += blockDim.x) {
+        float gam = (Z == NEG_INF) ? 0.f : ex2(g[j] - Z);
+        if (pdf_level) g[j] = gam;
+        else post[base + j] = gam;
+    }
+    if (!pdf_level) return;
+    __syncthreads();
+    const PdfMap &pm = G.pm;
+    const int so = pm.slot_off[gi];
+    const int *ps = pm.pdf_slot + (size_t)gi * D;
+    float *out = post + ((size_t)b * N_max + n) * D;
+    for (int d = tid; d < D; d += blockDim.x) {
+        int sl = ps[d];
+        float acc = 0.f;
+        if (sl >= 0)
+            for (int q = pm.slot_sptr[so + sl]; q < pm.slot_sptr[so + sl + 1]; ++q) acc += g[pm.slot_states[q]];
+        out[d] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ totals
+
+// loss_b = logZ_num − logZ_den (0 for flagged sequences) and the
+// fixed-order float64 totals {Σ loss, Σ N_b, Σ logZ_num, Σ logZ_den, n_bad}.
+__global__ void k_totals(const double *zn, const double *zd, const int *lengths, const int *status, int B,
+                         double *loss, double *totals) {
+    __shared__ double sh[5][256];
+    const int tid = threadIdx.x;
+    double t[5] = {0, 0, 0, 0, 0};
+    // each thread sums a contiguous chunk in ascending b; chunks combine in a fixed tree
+    const int chunk = (B + blockDim.x - 1) / blockDim.x;
+    for (int b = tid * chunk; b < min(B, (tid + 1) * chunk); ++b) {
+        if (status[b] == 0) {
+            double l = zn[b] - zd[b];
+            loss[b] = l;
+            t[0] += l;
+            t[1] += (double)lengths[b];
+            t[2] += zn[b];
+            t[3] += zd[b];
+        } else {
+            loss[b] = 0.0;
+            t[4] += 1.0;
+        }
+    }
+    for (int q = 0; q < 5; ++q) sh[q][tid] = t[q];
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+        if (tid < o)
+            for (int q = 0; q < 5; ++q) sh[q][tid] += sh[q][tid + o];
+        __syncthreads();
+    }
+    if (tid == 0)
+        for (int q = 0; q < 5; ++q) totals[q] = sh[q][0];
+}
+
+// ------------------------------------------------------------------ launch helpers
+
+using KFn = void (*)(FBArgs);
+
+template <bool BWD, int MODE>
+static KFn pick_spt(int spt) {
+    switch (spt) {
+        case 1: return k_fb<BWD, MODE, 1>;
+        case 2: return k_fb<BWD, MODE, 2>;
+        case 4: return k_fb<BWD, MODE, 4>;
+        default: return k_fb<BWD, MODE, 8>;
+    }
+}
+
+static KFn pick(bool bwd, int mode, int spt) {
+    if (bwd) return mode == MODE_FACTORED ? pick_spt<true, MODE_FACTORED>(spt) : pick_spt<true, MODE_EXACT>(spt);
+    return mode == MODE_FACTORED ? pick_spt<false, MODE_FACTORED>(spt) : pick_spt<false, MODE_EXACT>(spt);
+}
+
+static fb_status check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_cuda_error(what, (int)e); return FB_ERR_CUDA; }
+    return FB_OK;
+}
+
+static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s) {
+    const Graph &G = a.g;
+    const bool post = bwd && a.post_kind != POST_NONE;
+    size_t sm = smem_bytes(G, bwd, post);
+    KFn fn = pick(bwd, G.mode, G.spt);
+    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    {
+        ProfScope ps(bwd ? (G.G == 1 ? "k_fb_bwd[G=1]" : "k_fb_bwd[G=B]") : (G.G == 1 ? "k_fb_fwd[G=1]" : "k_fb_fwd[G=B]"), s);
+        fn<<<a.B, G.T, sm, s>>>(a);
+    }
+    return check_launch("k_fb launch");
+}
+
+static FBArgs base_args(fb_graph g, const float *emis, const int *lengths, int B, int N_max) {
+    FBArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.g = g->g;
+    a.emis = emis;
+    a.lengths = lengths;
+    a.B = B;
+    a.N_max = N_max;
+    a.D = g->g.D;
+    return a;
+}
+
+// side stream + events for the concurrent numerator pass of lfmmi_loss_grad
+struct SideRes {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static std::mutex g_side_mu;
+static SideRes g_side[64];
+
+static SideRes *side_res() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_side_mu);
+    SideRes &r = g_side[dev & 63];
+    if (!r.s) {
+        cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+    }
+    return &r;
+}
+
+struct WsLayout {
+    size_t den_alpha, num_alpha, gnum, zn, zd, nst, total;
+};
+static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+static WsLayout ws_layout(const Graph &num, const Graph &den, int B, int N_max) {
+    WsLayout w;
+    size_t o = 0;
+    w.den_alpha = o; o += a256((size_t)B * N_max * den.K_tot * 4);
+    w.num_alpha = o; o += a256((size_t)N_max * num.K_tot * 4);
+    w.gnum = o; o += a256((size_t)N_max * num.pm.U_tot * 4);
+    w.zn = o; o += a256((size_t)B * 8);
+    w.zd = o; o += a256((size_t)B * 8);
+    w.nst = o; o += a256((size_t)B * 4);
+    w.total = o;
+    return w;
+}
+
+}  // namespace fbx
+
+using namespace fbx;
+
+// ------------------------------------------------------------------ C ABI
+
+extern "C" fb_status fb_forward(fb_graph g, const float *log_emis, const int32_t *lengths, int32_t B,
+                                int32_t N_max, float *alpha, double *alpha_scale, double *logZ,
+                                int32_t *seq_status, void *stream) {
+    if (!g || !log_emis || !lengths || !logZ || !seq_status || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B)) return FB_ERR_INVALID_ARG;
+    if (alpha && !alpha_scale) return FB_ERR_INVALID_ARG;
+    FBArgs a = base_args(g, log_emis, lengths, B, N_max);
+    a.lat = alpha;
+    a.scale = alpha_scale;
+    a.logZ = logZ;
+    a.status = seq_status;
+    return launch_fb(false, a, (cudaStream_t)stream);
+}
+
+extern "C" fb_status fb_backward(fb_graph g, const float *log_emis, const int32_t *lengths, int32_t B,
+                                 int32_t N_max, float *beta, double *beta_scale, double *logZ_beta,
+                                 const float *alpha, float *post, int32_t pdf_level, int32_t *seq_status,
+                                 void *stream) {
+    if (!g || !log_emis || !lengths || !seq_status || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B)) return FB_ERR_INVALID_ARG;
+    if (post && !alpha) return FB_ERR_INVALID_ARG;
+    if (pdf_level != 0 && pdf_level != 1) return FB_ERR_INVALID_ARG;
+    FBArgs a = base_args(g, log_emis, lengths, B, N_max);
+    a.lat = beta;
+    a.scale = beta_scale;
+    a.logZ = logZ_beta;
+    a.status = seq_status;
+    a.alpha = alpha;
+    a.post = post;
+    a.post_kind = post ? (pdf_level ? POST_PDF_DENSE : POST_STATE) : POST_NONE;
+    return launch_fb(true, a, (cudaStream_t)stream);
+}
+
+extern "C" fb_status fb_posteriors(fb_graph g, const float *alpha, const float *beta, const int32_t *lengths,
+                                   const int32_t *seq_status, int32_t B, int32_t N_max, int32_t pdf_level,
+                                   float *post, void *stream) {
+    if (!g || !alpha || !beta || !lengths || !post || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B)) return FB_ERR_INVALID_ARG;
+    if (pdf_level != 0 && pdf_level != 1) return FB_ERR_INVALID_ARG;
+    const Graph &G = g->g;
+    cudaStream_t s = (cudaStream_t)stream;
+    size_t sm = (size_t)G.K_max * 4;
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_posteriors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    {
+        ProfScope ps("k_posteriors", s);
+        k_posteriors<<<(unsigned)((size_t)B * N_max), 256, sm, s>>>(G, alpha, beta, lengths, seq_status, B, N_max,
+                                                                  G.D, pdf_level, post);
+    }
+    return check_launch("k_posteriors launch");
+}
+
+extern "C" size_t fb_workspace_bytes(fb_graph num, fb_graph den, int32_t B, int32_t N_max) {
+    if (!num || !den || B < 1 || N_max < 1) return 0;
+    return ws_layout(num->g, den->g, B, N_max).total;
+}
+
+extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *log_emis, const int32_t *lengths,
+                                     int32_t B, int32_t N_max, float *grad, double *loss, double *totals,
+                                     int32_t *seq_status, void *workspace, size_t workspace_bytes,
+                                     void *stream) {
+    if (!num || !den || !log_emis || !lengths || !grad || !loss || !totals || !seq_status || B < 1 || N_max < 1)
+        return FB_ERR_INVALID_ARG;
+    if (num->g.G != B || den->g.G != 1 || num->g.D != den->g.D) return FB_ERR_INVALID_ARG;
+    WsLayout L = ws_layout(num->g, den->g, B, N_max);
+    if (!workspace || workspace_bytes < L.total) return FB_ERR_WORKSPACE;
+    unsigned char *ws = (unsigned char *)workspace;
+    float *den_alpha = (float *)(ws + L.den_alpha);
+    float *num_alpha = (float *)(ws + L.num_alpha);
+    float *gnum = (float *)(ws + L.gnum);
+    double *zn = (double *)(ws + L.zn), *zd = (double *)(ws + L.zd);
+    int *nst = (int *)(ws + L.nst);
+    cudaStream_t s = (cudaStream_t)stream;
+    SideRes *sr = side_res();
+    fb_status r;
+    // numerator pass on the side stream (runs on the SMs the B denominator CTAs leave idle)
+    cudaEventRecord(sr->fork, s);
+    cudaStreamWaitEvent(sr->s, sr->fork, 0);
+    {
+        FBArgs a = base_args(num, log_emis, lengths, B, N_max);
+        a.lat = num_alpha; a.logZ = zn; a.status = nst;
+        if ((r = launch_fb(false, a, sr->s)) != FB_OK) return r;
+        FBArgs c = base_args(num, log_emis, lengths, B, N_max);
+        c.status = nst; c.alpha = num_alpha; c.post = gnum; c.post_kind = POST_PDF_COMPACT;
+        if ((r = launch_fb(true, c, sr->s)) != FB_OK) return r;
+    }
+    cudaEventRecord(sr->join, sr->s);
+    // denominator forward on the caller's stream, concurrently
+    {
+        FBArgs a = base_args(den, log_emis, lengths, B, N_max);
+        a.lat = den_alpha; a.logZ = zd; a.status = seq_status;
+        if ((r = launch_fb(false, a, s)) != FB_OK) return r;
+    }
+    cudaStreamWaitEvent(s, sr->join, 0);
+    // denominator backward + fused posterior/gradient epilogue + loss
+    {
+        FBArgs c = base_args(den, log_emis, lengths, B, N_max);
+        c.status = seq_status; c.status2 = nst; c.alpha = den_alpha;
+        c.post = grad; c.post_kind = POST_GRAD;
+        c.gnum = gnum; c.num_slot_off = num->g.pm.slot_off; c.num_pdf_slot = num->g.pm.pdf_slot;
+        if ((r = launch_fb(true, c, s)) != FB_OK) return r;
+    }
+    {
+        ProfScope ps("k_totals", s);
+        k_totals<<<1, 256, 0, s>>>(zn, zd, lengths, seq_status, B, loss, totals);
+    }
+    return check_launch("k_totals launch");
+}
+
+extern "C" size_t fb_viterbi_workspace_bytes(fb_graph g, int32_t B, int32_t N_max) {
+    (void)g; (void)B; (void)N_max;
+    return 0;
+}
+
+extern "C" fb_status fb_viterbi(fb_graph g, const float *log_emis, const int32_t *lengths, int32_t B,
+                                int32_t N_max, double *score, int32_t *path, int32_t *seq_status,
+                                void *workspace, size_t workspace_bytes, void *stream) {
+    (void)g; (void)log_emis; (void)lengths; (void)B; (void)N_max; (void)score; (void)path;
+    (void)seq_status; (void)workspace; (void)workspace_bytes; (void)stream;
+    return FB_ERR_UNSUPPORTED;
+}
+
+extern "C" void fb_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_on = on != 0;
+}
+
+extern "C" void fb_profile_reset(void) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (auto &r : g_prof) { g_event_pool.push_back(r.a); g_event_pool.push_back(r.b); }
+    g_prof.clear();
+}
+
+extern "C" fb_status fb_profile_collect(const char **names, int64_t *counts, double *ms, int32_t cap, int32_t *n) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::vector<const char *> nm;
+    std::vector<int64_t> ct;
+    std::vector<double> tm;
+    for (auto &r : g_prof) {
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) { set_cuda_error("cudaEventSynchronize", (int)e); return FB_ERR_CUDA; }
+        float x = 0.f;
+        cudaEventElapsedTime(&x, r.a, r.b);
+        size_t i = 0;
+        for (; i < nm.size(); ++i)
+            if (std::strcmp(nm[i], r.name) == 0) break;
+        if (i == nm.size()) { nm.push_back(r.name); ct.push_back(0); tm.push_back(0.0); }
+        ct[i] += 1;
+        tm[i] += x;
+    }
+    int m = (int)std::min<size_t>(nm.size(), (size_t)std::max(0, cap));
+    for (int i = 0; i < m; ++i) {
+        if (names) names[i] = nm[i];
+        if (counts) counts[i] = ct[i];
+        if (ms) ms[i] = tm[i];
+    }
+    if (n) *n = m;
+    return FB_OK;
+}
+
+extern "C" const char *fb_status_str(fb_status s) {
+    switch (s) {
+        case FB_OK: return "ok";
+        case FB_ERR_INVALID_ARG: return "invalid argument";
+        case FB_ERR_SHAPE: return "shape mismatch";
+        case FB_ERR_INVALID_GRAPH: return "invalid graph";
+        case FB_ERR_CUDA: return "CUDA error";
+        case FB_ERR_NOMEM: return "out of device memory";
+        case FB_ERR_WORKSPACE: return "workspace too small";
+        case FB_ERR_UNSUPPORTED: return "unsupported graph size for this build";
+    }
+    return "unknown status";
+}
+
+extern "C" const char *fb_last_cuda_error(void) {
+    std::lock_guard<std::mutex> lk(g_err_mu);
+    return g_err.c_str();
+}

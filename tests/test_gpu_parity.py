@@ -1,0 +1,261 @@
+"""T1-T3: CUDA path (through the C-ABI) vs the float64 oracle, element by element.
+
+Gates (BASELINE.json north_star): |ΔlogZ| ≤ 1e-5·max(1, |logZ|); max |Δγ| ≤ 1e-5;
+max |Δgrad| ≤ 1e-5.  Inputs are generated once in fp32 and fed bit-identically
+to both sides.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2112_00709_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL_LOGZ = 1e-5
+TOL_POST = 1e-5
+TOL_GRAD = 1e-5
+
+
+@pytest.fixture(scope="module")
+def fbx():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    from paper_2112_00709_b200 import build
+
+    build.build()
+    import paper_2112_00709_b200 as fbx
+
+    fbx.lib()
+    return fbx
+
+
+def dev(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_fb(fbx, graph, emis, lengths, flags=0, post="state"):
+    import torch
+
+    g = fbx.Graph.from_host(graph, flags)
+    e, L = dev(emis), dev(lengths.astype(np.int32))
+    logZ, alpha, scale, st = fbx.fb_forward(g, e, L)
+    p, logZb, st2, beta, bscale = fbx.fb_backward(g, e, L, alpha=alpha, status=st.clone(), want_beta=True, post=post)
+    torch.cuda.synchronize()
+    return dict(g=g, logZ=logZ.cpu().numpy(), logZb=logZb.cpu().numpy(), st=st2.cpu().numpy(),
+                st_fwd=st.cpu().numpy(), post=p.cpu().numpy(), alpha=alpha, scale=scale, beta=beta,
+                bscale=bscale, e=e, L=L)
+
+
+def check_logZ(got, ref, ok):
+    err = np.abs(got[ok] - ref[ok]) / np.maximum(1.0, np.abs(ref[ok]))
+    assert err.max(initial=0) <= TOL_LOGZ, err.max()
+    return err.max(initial=0)
+
+
+# ------------------------------------------------------------------ C1 (100 seeds, dense K=3)
+
+@pytest.mark.parametrize("flags", [0, 1])
+def test_c1_vs_oracle_and_bruteforce(fbx, flags):
+    ws = [synth.make_c1(s) for s in range(100)]
+    comp = synth.compose([w.den for w in ws])
+    emis = np.concatenate([w.emis for w in ws])
+    lens = np.full(100, 6, np.int32)
+    r = run_fb(fbx, comp, emis, lens, flags=flags)
+    ref = oracle.fb_batch(comp, emis, lens, post=True)
+    assert (r["st"] == 0).all()
+    check_logZ(r["logZ"], ref["logZ"], np.ones(100, bool))
+    check_logZ(r["logZb"], ref["logZ"], np.ones(100, bool))
+    assert np.abs(r["post"] - ref["post"]).max() <= TOL_POST
+
+
+# ------------------------------------------------------------------ C2 numerator graphs (G = B)
+
+@pytest.mark.parametrize("kind", ["uniform", "softmax4"])
+def test_c2_numerators(fbx, kind):
+    w = synth.make_c2(seed=2, kind=kind)
+    comp = synth.compose(w.nums)
+    r = run_fb(fbx, comp, w.emis, w.lengths)
+    ref = oracle.fb_batch(comp, w.emis, w.lengths, alpha=True, post=True)
+    assert (r["st"] == ref["status"]).all() and (r["st"] == 0).all()
+    check_logZ(r["logZ"], ref["logZ"], r["st"] == 0)
+    err = np.abs(r["post"] - ref["post"]).max()
+    assert err <= TOL_POST, err
+    # lattice: α_true = α̂ + scale on states carrying mass
+    alpha = r["alpha"].cpu().numpy()
+    scale = r["scale"].cpu().numpy()
+    so = comp.state_offsets
+    for b in range(0, w.B, 7):
+        K = so[b + 1] - so[b]
+        N = w.lengths[b]
+        a_gpu = alpha[w.N_max * so[b]: w.N_max * so[b + 1]].reshape(w.N_max, K)
+        a_ref = ref["alpha"][w.N_max * so[b]: w.N_max * so[b + 1]].reshape(w.N_max, K)
+        rel = a_ref[:N] - scale[b, :N, None]
+        live = (r["post"][w.N_max * so[b]: w.N_max * so[b + 1]].reshape(w.N_max, K)[:N] > 1e-6)
+        assert np.abs(a_gpu[:N][live] - rel[live]).max() <= 1e-3
+        assert np.isneginf(a_gpu[N:]).all()
+
+
+# ------------------------------------------------------------------ C3 denominator (G = 1), reduced
+
+@pytest.mark.parametrize("kind,flags", [("uniform", 0), ("softmax4", 0), ("uniform", 1), ("softmax8", 0)])
+def test_c3_den_reduced(fbx, kind, flags):
+    w = synth.make_c3(seed=3, B=6, N=64, kind=kind)
+    lens = np.array([64, 1, 33, 64, 17, 50], np.int32)
+    r = run_fb(fbx, w.den, w.emis, lens, flags=flags)
+    ref = oracle.fb_batch(w.den, w.emis, lens, post=True)
+    assert (r["st"] == 0).all()
+    check_logZ(r["logZ"], ref["logZ"], np.ones(6, bool))
+    err = np.abs(r["post"].reshape(ref["post"].shape) - ref["post"]).max()
+    tol = TOL_POST if kind != "softmax8" else 3 * TOL_POST  # σ = 8 is a reported stress case
+    assert err <= tol, err
+    # posteriors sum to 1 on valid frames, 0 on padding
+    P = r["post"].reshape(6, 64, -1)
+    for b in range(6):
+        assert np.abs(P[b, : lens[b]].sum(1) - 1).max() <= 1e-4
+        assert (P[b, lens[b]:] == 0).all()
+
+
+def test_c3_pdf_level_and_standalone_posteriors(fbx):
+    w = synth.make_c4(seed=4, B=4, N=40)
+    den = w.den
+    lens = np.array([40, 40, 12, 3], np.int32)
+    r = run_fb(fbx, den, w.emis, lens, post="pdf")
+    ref = oracle.fb_batch(den, w.emis, lens, post=True, post_pdf=True)
+    assert np.abs(r["post"] - ref["post_pdf"]).max() <= TOL_POST
+    st = dev(r["st"])
+    p_state = fbx.fb_posteriors(r["g"], r["alpha"], r["beta"], r["L"], st, 4, 40, pdf_level=False)
+    p_pdf = fbx.fb_posteriors(r["g"], r["alpha"], r["beta"], r["L"], st, 4, 40, pdf_level=True)
+    assert np.abs(p_state.cpu().numpy().reshape(ref["post"].shape) - ref["post"]).max() <= TOL_POST
+    assert np.abs(p_pdf.cpu().numpy() - ref["post_pdf"]).max() <= TOL_POST
+
+
+# ------------------------------------------------------------------ C4 LF-MMI, reduced
+
+@pytest.mark.parametrize("kind", ["uniform", "softmax4"])
+def test_c4_lfmmi_reduced(fbx, kind):
+    import torch
+
+    w = synth.make_c4(seed=4, B=8, N=120, kind=kind, L_range=(20, 60))
+    lens = np.array([120, 120, 90, 61, 120, 100, 75, 120], np.int32)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(w.emis), dev(lens))
+    torch.cuda.synchronize()
+    ref = oracle.lfmmi_batch(synth.compose(w.nums), synth.compose([w.den]), w.emis, lens)
+    st = st.cpu().numpy()
+    assert (st == ref["status"]).all()
+    ok = st == 0
+    assert ok.sum() >= 6
+    zd_ref, zn_ref = ref["logZ_den"], ref["logZ_num"]
+    err_loss = np.abs(loss.cpu().numpy()[ok] - ref["loss"][ok]) / np.maximum(1, np.abs(zd_ref[ok]))
+    assert err_loss.max() <= TOL_LOGZ
+    g = grad.cpu().numpy()
+    err = np.abs(g - ref["grad"]).max()
+    assert err <= TOL_GRAD, err
+    t = totals.cpu().numpy()
+    assert t[4] == (~ok).sum() and t[1] == lens[ok].sum()
+    assert abs(t[0] - ref["totals"][0]) <= 1e-5 * max(1, abs(ref["totals"][3]))
+    # per-frame zero sum of the gradient (AC5)
+    assert np.abs(g.sum(-1)).max() <= 1e-4
+
+
+# ------------------------------------------------------------------ faults (T3)
+
+def test_status_flags(fbx):
+    import torch
+
+    w = synth.make_c4(seed=14, B=4, N=30, L_range=(10, 20))
+    emis = w.emis.copy()
+    emis[1, 5, :] = np.nan
+    lens = np.array([30, 30, 0, 31], np.int32)  # bad lengths: 0 and > N_max
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(emis), dev(lens))
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    assert st[0] == 0
+    assert st[1] & fbx.SEQ_NONFINITE_INPUT
+    assert st[2] & fbx.SEQ_BAD_LENGTH and st[3] & fbx.SEQ_BAD_LENGTH
+    g = grad.cpu().numpy()
+    assert (g[1:] == 0).all() and np.isfinite(g).all()
+    assert (loss.cpu().numpy()[1:] == 0).all()
+    assert totals.cpu().numpy()[4] == 3
+
+
+def test_empty_lattice(fbx):
+    # numerator needs ≥ L frames; give it fewer
+    rng = np.random.Generator(np.random.PCG64(5))
+    g = synth.numerator_graph(rng, 20, 50, "identity")
+    emis = synth.emissions(rng, 2, 30, 50)
+    lens = np.array([10, 30], np.int32)
+    r = run_fb(fbx, synth.compose([g, g]), emis, lens)
+    assert r["st_fwd"][0] == fbx.SEQ_EMPTY_LATTICE and r["st_fwd"][1] == 0
+    assert r["logZ"][0] == -np.inf
+    ref = oracle.fb_batch(synth.compose([g, g]), emis, lens)
+    check_logZ(r["logZ"], ref["logZ"], np.array([False, True]))
+
+
+# ------------------------------------------------------------------ determinism (T2)
+
+def test_bitwise_determinism_and_batch_independence(fbx):
+    import torch
+
+    w = synth.make_c3(seed=9, B=5, N=40)
+    lens = np.array([40, 31, 40, 7, 22], np.int32)
+    r1 = run_fb(fbx, w.den, w.emis, lens)
+    r2 = run_fb(fbx, w.den, w.emis, lens)
+    assert (r1["post"] == r2["post"]).all() and (r1["logZ"] == r2["logZ"]).all()
+    # sequence 3 alone (B = 1) == its row in the batch, bit for bit
+    solo = run_fb(fbx, w.den, w.emis[3:4].copy(), lens[3:4])
+    K = w.den.K
+    assert (solo["post"].reshape(1, 40, K) == r1["post"].reshape(5, 40, K)[3:4]).all()
+    assert solo["logZ"][0] == r1["logZ"][3]
+    # shuffled batch → permuted identical outputs
+    perm = np.array([4, 2, 0, 3, 1])
+    r3 = run_fb(fbx, w.den, w.emis[perm].copy(), lens[perm])
+    assert (r3["post"].reshape(5, 40, K) == r1["post"].reshape(5, 40, K)[perm]).all()
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, sampled
+
+@pytest.mark.slow
+def test_c3_full_size_sampled(fbx):
+    """C3 at its full size (B=128, N=500, K=3000, nnz≈20k) in the bench launch
+    configuration; the oracle recomputes sampled utterances one by one."""
+    w = synth.make_c3(seed=3)
+    r = run_fb(fbx, w.den, w.emis, w.lengths)
+    assert (r["st"] == 0).all()
+    K = w.den.K
+    P = r["post"].reshape(128, 500, K)
+    for b in (0, 77, 127):
+        ref = oracle.fb_batch(w.den, w.emis[b:b + 1], w.lengths[b:b + 1], post=True)
+        check_logZ(r["logZ"][b:b + 1], ref["logZ"], np.ones(1, bool))
+        assert np.abs(P[b] - ref["post"][0]).max() <= TOL_POST
+    # properties that hold at any size, on every utterance
+    assert np.abs(P.sum(-1) - 1).max() <= 1e-4
+    assert (np.abs(r["logZ"] - r["logZb"]) / np.abs(r["logZ"])).max() <= TOL_LOGZ
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled(fbx):
+    import torch
+
+    w = synth.make_c4(seed=4)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(w.emis), dev(w.lengths))
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    assert (st == 0).all()
+    g = grad.cpu().numpy()
+    for b in (3, 64, 120):
+        ref = oracle.lfmmi_batch(synth.compose([w.nums[b]]), synth.compose([w.den]), w.emis[b:b + 1],
+                                 w.lengths[b:b + 1])
+        assert abs(loss.cpu().numpy()[b] - ref["loss"][0]) <= TOL_LOGZ * max(1, abs(ref["logZ_den"][0]))
+        assert np.abs(g[b] - ref["grad"][0]).max() <= TOL_GRAD
+    assert np.abs(g.sum(-1)).max() <= 1e-4
