@@ -162,14 +162,16 @@ bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
 }  // namespace
 
 size_t smem_bytes(const Graph &g, bool backward, bool post) {
+    // must match carve<V>() in fb_kernels.cu; V = double in exact mode
     const Sched &s = backward ? g.bwd : g.fwd;
+    const size_t vsz = g.mode == MODE_EXACT ? 8 : 4;
     size_t b = 0;
-    b += align16((size_t)s.rows_max * 32 * 8);                  // arc records
-    b += align16((size_t)g.K_max * 4);                          // u (log2 domain)
-    if (g.mode == MODE_FACTORED) b += align16((size_t)g.K_max * 4);  // p = exp2(u)
-    b += align16((size_t)std::max(1, s.nseg_max) * 4);          // segment partials
-    if (backward && post) b += align16((size_t)g.K_max * 4);    // γ row for the pdf gather
-    b += align16(4 * (2 * 32 + 2 * 64 + 32));                  // reductions + flags
+    b += align16((size_t)s.rows_max * 32 * 8);                        // arc records
+    b += align16((size_t)g.K_max * vsz);                              // u (log2 domain)
+    if (g.mode == MODE_FACTORED) b += align16((size_t)g.K_max * 4);   // p = exp2(u)
+    b += align16((size_t)std::max(1, s.nseg_max) * vsz);              // segment partials
+    if (backward && post) b += align16((size_t)g.K_max * 4);          // γ row for the pdf gather
+    b += align16(8 * (2 * 32 + 2 * 64) + 64);                         // reductions + flags
     return b;
 }
 
@@ -239,10 +241,15 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
             nnz_min = std::min<long long>(nnz_min, row_ptr[state_offsets[g + 1]] - row_ptr[state_offsets[g]]);
         gr.mode = (factored_ok && nnz_min >= 4096) ? MODE_FACTORED : MODE_EXACT;
     }
-    // threads per CTA and states per thread
-    int T = gr.nnz_max >= 16384 ? 1024 : std::min(1024, std::max(32, pow2ceil((gr.nnz_max + 15) / 16)));
+    // threads per CTA and states per thread: factored (large ergodic) graphs use
+    // 1024 threads (~20 arcs per thread per frame); exact-mode graphs are short
+    // dependent chains, so they get ~4 arcs per thread to cut per-frame latency.
+    int T;
+    if (gr.mode == MODE_FACTORED)
+        T = gr.nnz_max >= 16384 ? 1024 : std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 15) / 16)));
+    else
+        T = std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 3) / 4)));
     T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
-    T = std::max(T, 32);
     int spt = pow2ceil((gr.K_max + T - 1) / T);
     if (spt > kMaxSPT) return FB_ERR_UNSUPPORTED;
     gr.T = T;

@@ -32,6 +32,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "fb_internal.h"
@@ -95,6 +96,7 @@ struct ProfScope {
 // ------------------------------------------------------------------ device helpers
 
 #define NEG_INF (-__int_as_float(0x7f800000))
+#define NEG_INF_D (-__longlong_as_double(0x7ff0000000000000ll))
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -106,22 +108,36 @@ __device__ __forceinline__ float lg2(float x) {
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-__device__ __forceinline__ float warp_max(float v) {
+template <class V>
+__device__ __forceinline__ V ninf() { return (V)NEG_INF_D; }
+template <class V>
+__device__ __forceinline__ V vmax(V a, V b) { return a > b ? a : (b > a ? b : a); }
+template <class V>
+__device__ __forceinline__ V vmin(V a, V b) { return a < b ? a : (b < a ? b : a); }
+template <class V>
+__device__ __forceinline__ V warp_max(V v) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o; o >>= 1) v = vmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
-// (m, s) log-sum-exp pair combine: value = m + log2(s)
-__device__ __forceinline__ void lse_combine(float &m, float &s, float m2, float s2) {
-    float M = fmaxf(m, m2);
-    if (M == NEG_INF) { m = NEG_INF; s = 0.f; return; }
-    s = (m == NEG_INF ? 0.f : s * ex2(m - M)) + (m2 == NEG_INF ? 0.f : s2 * ex2(m2 - M));
+// (m, s) log-sum-exp pair (value = m + log2 s), m in V, s in float (s ∈ [1, n])
+template <class V>
+__device__ __forceinline__ void lse_push(V &m, float &s, V x) {
+    if (x > m) { s = (m == ninf<V>() ? 0.f : s * ex2((float)(m - x))) + 1.f; m = x; }
+    else if (x != ninf<V>()) s += ex2((float)(x - m));
+}
+template <class V>
+__device__ __forceinline__ void lse_combine(V &m, float &s, V m2, float s2) {
+    V M = vmax(m, m2);
+    if (M == ninf<V>()) { m = ninf<V>(); s = 0.f; return; }
+    s = (m == ninf<V>() ? 0.f : s * ex2((float)(m - M))) + (m2 == ninf<V>() ? 0.f : s2 * ex2((float)(m2 - M)));
     m = M;
 }
-__device__ __forceinline__ void warp_lse(float &m, float &s) {
+template <class V>
+__device__ __forceinline__ void warp_lse(V &m, float &s) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+        V m2 = __shfl_xor_sync(0xffffffffu, m, o);
         float s2 = __shfl_xor_sync(0xffffffffu, s, o);
         lse_combine(m, s, m2, s2);
     }
@@ -129,15 +145,12 @@ __device__ __forceinline__ void warp_lse(float &m, float &s) {
 __device__ __forceinline__ size_t align16d(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Online max-then-sum over one segment, re-reading its records (fallback path
-// of factored mode; weights stored as e^{T} there).
-__device__ __noinline__ float exact_segment(const uint2 *col, int s_begin, int s_end, const float *u,
-                                            bool factored) {
+// of factored mode, where weights are stored as e^{T}).  Accurate libm ops.
+__device__ __noinline__ float exact_segment(const uint2 *col, int s_begin, int s_end, const float *u) {
     float m = NEG_INF, sum = 0.f;
     for (int s = s_begin; s <= s_end; ++s) {
         uint2 r = col[s * 32];
-        float w = __uint_as_float(r.y);
-        if (factored) w = log2f(w);
-        float x = u[r.x & 0xFFFFu] + w;
+        float x = u[r.x & 0xFFFFu] + log2f(__uint_as_float(r.y));
         if (x == NEG_INF) continue;
         if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
         else sum += exp2f(x - m);
@@ -168,62 +181,75 @@ struct FBArgs {
     const int *num_pdf_slot; // [B*D]
 };
 
+// Shared-memory carve-up; must match smem_bytes() in fb_graph.cpp.
+template <class V>
 struct Smem {
     uint2 *rec;
-    float *u, *p, *part, *gbuf, *wmax, *wz;
+    V *u;
+    float *p;
+    V *part;
+    float *gbuf;
+    double *wmax;  // [2][32]
+    double *wz;    // [2][32][2]  (m, s) per warp
     int *flag;
 };
 
-__device__ __forceinline__ Smem carve(unsigned char *base, const Graph &G, bool bwd, bool post, int mode) {
+template <class V>
+__device__ __forceinline__ Smem<V> carve(unsigned char *base, const Graph &G, bool bwd, bool post, int mode) {
     const Sched &S = bwd ? G.bwd : G.fwd;
-    Smem m;
+    Smem<V> m;
     size_t off = 0;
     m.rec = (uint2 *)(base + off); off += align16d((size_t)S.rows_max * 32 * 8);
-    m.u = (float *)(base + off); off += align16d((size_t)G.K_max * 4);
+    m.u = (V *)(base + off); off += align16d((size_t)G.K_max * sizeof(V));
     m.p = nullptr;
     if (mode == MODE_FACTORED) { m.p = (float *)(base + off); off += align16d((size_t)G.K_max * 4); }
-    m.part = (float *)(base + off); off += align16d((size_t)max(1, S.nseg_max) * 4);
+    m.part = (V *)(base + off); off += align16d((size_t)max(1, S.nseg_max) * sizeof(V));
     m.gbuf = nullptr;
     if (bwd && post) { m.gbuf = (float *)(base + off); off += align16d((size_t)G.K_max * 4); }
-    m.wmax = (float *)(base + off);
+    m.wmax = (double *)(base + off);
     m.wz = m.wmax + 64;
     m.flag = (int *)(m.wz + 128);
     return m;
 }
 
-// Block-wide max of per-warp maxima stored in w[0..W-1] (every warp computes it).
-__device__ __forceinline__ float block_max_from(const float *w, int W, int lane) {
-    float v = lane < W ? w[lane] : NEG_INF;
+// Block-wide reductions over per-warp partials w[0..W-1] (every warp computes them).
+template <class V>
+__device__ __forceinline__ V block_max_from(const double *w, int W, int lane) {
+    V v = lane < W ? (V)w[lane] : ninf<V>();
     return warp_max(v);
 }
-__device__ __forceinline__ float block_lse_from(const float *wz, int W, int lane) {
-    float m = lane < W ? wz[2 * lane] : NEG_INF;
-    float s = lane < W ? wz[2 * lane + 1] : 0.f;
+template <class V>
+__device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
+    V m = lane < W ? (V)wz[2 * lane] : ninf<V>();
+    float s = lane < W ? (float)wz[2 * lane + 1] : 0.f;
     warp_lse(m, s);
-    return m == NEG_INF ? NEG_INF : m + lg2(s);
+    return m == ninf<V>() ? ninf<V>() : m + (V)lg2(s);
 }
 
 // Combine the log2 partials of one state's segments.
-__device__ __forceinline__ float combine_segments(const float *part, int packed) {
+template <class V>
+__device__ __forceinline__ V combine_segments(const V *part, int packed) {
     int seg0 = packed & 0xFFFF, ns = packed >> 16;
-    if (ns == 0) return NEG_INF;
-    float y = part[seg0];
+    if (ns == 0) return ninf<V>();
+    V y = part[seg0];
     if (ns == 1) return y;
-    float m = y;
-    for (int q = 1; q < ns; ++q) m = fmaxf(m, part[seg0 + q]);
-    if (m == NEG_INF) return NEG_INF;
+    V m = y;
+    for (int q = 1; q < ns; ++q) m = vmax(m, part[seg0 + q]);
+    if (m == ninf<V>()) return m;
     float s = 0.f;
-    for (int q = 0; q < ns; ++q) s += ex2(part[seg0 + q] - m);
-    return m + lg2(s);
+    for (int q = 0; q < ns; ++q) s += ex2((float)(part[seg0 + q] - m));
+    return m + (V)lg2(s);
 }
 
 // Phase A: reduce this lane's slot column into the segment partials.
-template <int MODE>
-__device__ __forceinline__ void phase_a(const uint2 *col, int cnt, const float *u, const float *p, float *part) {
+//  factored: Σ p_src · e^{T} (one FMA per arc), exact fallback outside [2^-80, 2^120];
+//  exact:    online max-then-sum in V (double for exact mode) with one ex2 per arc.
+template <int MODE, class V>
+__device__ __forceinline__ void phase_a(const uint2 *col, int cnt, const V *u, const float *p, V *part) {
     constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
     constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
-    int seg_start = 0;
     if (MODE == MODE_FACTORED) {
+        int seg_start = 0;
         float acc = 0.f;
         for (int s = 0; s < cnt; s += 4) {
             uint2 r[4];
@@ -238,9 +264,10 @@ __device__ __forceinline__ void phase_a(const uint2 *col, int cnt, const float *
                     acc = fmaf(pv[q], __uint_as_float(r[q].y), acc);
                     unsigned sg = r[q].x >> 16;
                     if (sg) {
-                        float val = (acc >= kTiny && acc <= kHuge) ? lg2(acc)
-                                                                   : exact_segment(col, seg_start, s + q, u, true);
-                        part[sg - 1] = val;
+                        float val = (acc >= kTiny && acc <= kHuge)
+                                        ? lg2(acc)
+                                        : exact_segment(col, seg_start, s + q, (const float *)u);
+                        part[sg - 1] = (V)val;
                         acc = 0.f;
                         seg_start = s + q + 1;
                     }
@@ -248,10 +275,11 @@ __device__ __forceinline__ void phase_a(const uint2 *col, int cnt, const float *
             }
         }
     } else {
-        float m = NEG_INF, sum = 0.f;
+        V m = ninf<V>();
+        float sum = 0.f;
         for (int s = 0; s < cnt; s += 4) {
             uint2 r[4];
-            float uv[4];
+            V uv[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) r[q] = (s + q < cnt) ? col[(s + q) * 32] : make_uint2(0u, 0u);
 #pragma unroll
@@ -259,15 +287,15 @@ __device__ __forceinline__ void phase_a(const uint2 *col, int cnt, const float *
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (s + q < cnt) {
-                    float x = uv[q] + __uint_as_float(r[q].y);
-                    float hi = fmaxf(m, x), lo = fminf(m, x);
-                    float e = (lo == NEG_INF) ? 0.f : ex2(lo - hi);
+                    V x = uv[q] + (V)__uint_as_float(r[q].y);
+                    V hi = vmax(m, x), lo = vmin(m, x);
+                    float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
                     sum = (x > m) ? fmaf(sum, e, 1.f) : sum + e;
                     m = hi;
                     unsigned sg = r[q].x >> 16;
                     if (sg) {
-                        part[sg - 1] = (m == NEG_INF) ? NEG_INF : m + lg2(sum);
-                        m = NEG_INF;
+                        part[sg - 1] = (m == ninf<V>()) ? m : m + (V)lg2(sum);
+                        m = ninf<V>();
                         sum = 0.f;
                     }
                 }
@@ -296,10 +324,9 @@ __device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, int 
     const int *ps = pm.pdf_slot + (size_t)gi * D;
     const float *gn = nullptr;
     const int *nps = nullptr;
-    int nU = 0;
     if (a.post_kind == POST_GRAD) {
         const int nso = a.num_slot_off[b];
-        nU = a.num_slot_off[b + 1] - nso;
+        const int nU = a.num_slot_off[b + 1] - nso;
         gn = a.gnum + (size_t)a.N_max * nso + (size_t)n * nU;
         nps = a.num_pdf_slot + (size_t)b * D;
     }
@@ -341,8 +368,9 @@ __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, in
 
 // ------------------------------------------------------------------ forward / backward kernel
 
-template <bool BWD, int MODE, int SPT>
-__global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
+template <bool BWD, int MODE, int SPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArgs a) {
+    using V = typename std::conditional<MODE == MODE_EXACT, double, float>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Graph &G = a.g;
     const int b = blockIdx.x;
@@ -354,7 +382,9 @@ __global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
     const Sched &S = BWD ? G.bwd : G.fwd;
     const bool want_post = BWD && a.post_kind != POST_NONE;
     const bool pdf_post = want_post && a.post_kind != POST_STATE;
-    Smem sm = carve(smem_raw, G, BWD, want_post, MODE);
+    Smem<V> sm = carve<V>(smem_raw, G, BWD, want_post, MODE);
+    const V L2E = (V)1.4426950408889634;
+    const V LN2 = (V)0.6931471805599453;
 
     int st = 0;
     if (BWD) {
@@ -428,8 +458,8 @@ __global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
 
     float vcur[SPT], vnxt[SPT];   // emissions of the frame being produced and the next one
     float acur[SPT], anxt[SPT];   // α̂ prefetch (backward epilogue)
-    float cand[SPT], ucand[SPT];  // new α̂ / β̂ candidates and (bwd) v + β̂
-    float xpost[SPT];             // α̂_n + β̂_n of the frame whose posterior is pending
+    V cand[SPT], ucand[SPT];      // new α̂ / β̂ candidates and (bwd) v + β̂
+    V xpost[SPT];                 // α̂_n + β̂_n of the frame whose posterior is pending
     const int dir = BWD ? -1 : 1;
     const int n_first = BWD ? N - 1 : 0;
     load_v(n_first, vcur);
@@ -443,69 +473,69 @@ __global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
 
     // ---- frame n_first: π ⊗ v_0 (fwd, L6) / β̂_{N-1} = ω (bwd, L7)
     {
-        float lmax = NEG_INF;
+        V lmax = ninf<V>();
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             int j = tid + k * T;
-            if (j >= K) { cand[k] = NEG_INF; ucand[k] = NEG_INF; continue; }
+            if (j >= K) { cand[k] = ninf<V>(); ucand[k] = ninf<V>(); continue; }
             float v = vcur[k];
             if (!(v < INFINITY)) bad = true;
-            float v2 = v * kL2E;
+            V v2 = (V)v * L2E;
             if (!BWD) {
-                cand[k] = viable(k, 0) ? G.init2[s0 + j] + v2 : NEG_INF;
-                lmax = fmaxf(lmax, cand[k]);
+                cand[k] = viable(k, 0) ? (V)G.init2[s0 + j] + v2 : ninf<V>();
+                lmax = vmax(lmax, cand[k]);
             } else {
-                cand[k] = viable(k, N - 1) ? G.final2[s0 + j] : NEG_INF;
+                cand[k] = viable(k, N - 1) ? (V)G.final2[s0 + j] : ninf<V>();
                 ucand[k] = cand[k] + v2;
-                lmax = fmaxf(lmax, ucand[k]);
+                lmax = vmax(lmax, ucand[k]);
             }
         }
         lmax = warp_max(lmax);
-        if (lane == 0) sm.wmax[warp] = lmax;
+        if (lane == 0) sm.wmax[warp] = (double)lmax;
     }
     __syncthreads();
     int n = n_first;
     for (int step = 0;; ++step) {
         // ---- phase B2 of frame n: normalise, store, refresh u/p
         {
-            float c = block_max_from(sm.wmax + (step & 1) * 32, W, lane);
-            if (c == NEG_INF) c = 0.f;  // no viable state: keep 0̄ everywhere
+            V c = block_max_from<V>(sm.wmax + (step & 1) * 32, W, lane);
+            if (c == ninf<V>()) c = (V)0;  // no viable state: keep 0̄ everywhere
             scale += (double)c;
             if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
-            float zm = NEG_INF, zs = 0.f;
+            V zm = ninf<V>();
+            float zs = 0.f;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
                 int j = tid + k * T;
                 if (j >= K) continue;
-                float h = cand[k] - c;   // α̂_n or β̂_n (log2)
-                float uu = BWD ? ucand[k] - c : h;
-                if (a.lat) a.lat[lat_base + (size_t)n * K + j] = h * (float)kLN2;
+                V h = cand[k] - c;   // α̂_n or β̂_n (log2)
+                V uu = BWD ? ucand[k] - c : h;
+                if (a.lat) a.lat[lat_base + (size_t)n * K + j] = (float)(h * LN2);
                 sm.u[j] = uu;
-                if (MODE == MODE_FACTORED) sm.p[j] = ex2(uu);
+                if (MODE == MODE_FACTORED) sm.p[j] = ex2((float)uu);
                 ucand[k] = uu;
                 if (want_post) {
-                    float x = acur[k] * kL2E + h;
+                    V x = (V)acur[k] * L2E + h;
                     xpost[k] = x;
-                    if (x > zm) { zs = (zm == NEG_INF ? 0.f : zs * ex2(zm - x)) + 1.f; zm = x; }
-                    else if (x != NEG_INF) zs += ex2(x - zm);
+                    lse_push(zm, zs, x);
                 }
             }
             if (want_post) {
                 warp_lse(zm, zs);
-                if (lane == 0) { sm.wz[(step & 1) * 64 + 2 * warp] = zm; sm.wz[(step & 1) * 64 + 2 * warp + 1] = zs; }
+                if (lane == 0) {
+                    sm.wz[(step & 1) * 64 + 2 * warp] = (double)zm;
+                    sm.wz[(step & 1) * 64 + 2 * warp + 1] = (double)zs;
+                }
             }
         }
         const int n_next = n + dir;
         const bool last = BWD ? (n_next < 0) : (n_next >= N);
         __syncthreads();
-        if (last) {
-            if (want_post) { pend = true; pend_n = n; }
-            break;
-        }
         if (want_post) { pend = true; pend_n = n; }
+        if (last) break;
         // rotate prefetch: frame n_next becomes current, issue n_next + dir
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) { vcur[k] = vnxt[k]; }
+        for (int k = 0; k < SPT; ++k) vcur[k] = vnxt[k];
         load_v(n_next + dir, vnxt);
         if (want_post) {
 #pragma unroll
@@ -514,42 +544,42 @@ __global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
         }
         n = n_next;
         // ---- phase A of frame n
-        phase_a<MODE>(mycol, mycnt, sm.u, sm.p, sm.part);
+        phase_a<MODE, V>(mycol, mycnt, sm.u, sm.p, sm.part);
         __syncthreads();
         // ---- phase B1 of frame n (+ pending posterior of frame n - dir)
         {
             if (pend) {
-                float Z = block_lse_from(sm.wz + ((step) & 1) * 64, W, lane);
+                V Z = block_lse_from<V>(sm.wz + (step & 1) * 64, W, lane);
 #pragma unroll
                 for (int k = 0; k < SPT; ++k) {
                     int j = tid + k * T;
                     if (j >= K) continue;
-                    float gam = (Z == NEG_INF) ? 0.f : ex2(xpost[k] - Z);
+                    float gam = (Z == ninf<V>()) ? 0.f : ex2((float)(xpost[k] - Z));
                     if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pend_n * K + j] = gam;
                     else sm.gbuf[j] = gam;
                 }
             }
-            float lmax = NEG_INF;
+            V lmax = ninf<V>();
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
                 int j = tid + k * T;
-                if (j >= K) { cand[k] = NEG_INF; ucand[k] = NEG_INF; continue; }
-                float y = combine_segments(sm.part, segp[k]);
+                if (j >= K) { cand[k] = ninf<V>(); ucand[k] = ninf<V>(); continue; }
+                V y = combine_segments<V>(sm.part, segp[k]);
                 float v = vcur[k];
                 if (!(v < INFINITY)) bad = true;
-                float v2 = v * kL2E;
+                V v2 = (V)v * L2E;
                 bool ok = viable(k, n);
                 if (!BWD) {
-                    cand[k] = ok ? y + v2 : NEG_INF;
-                    lmax = fmaxf(lmax, cand[k]);
+                    cand[k] = ok ? y + v2 : ninf<V>();
+                    lmax = vmax(lmax, cand[k]);
                 } else {
-                    cand[k] = ok ? y : NEG_INF;
+                    cand[k] = ok ? y : ninf<V>();
                     ucand[k] = cand[k] + v2;
-                    lmax = fmaxf(lmax, ucand[k]);
+                    lmax = vmax(lmax, ucand[k]);
                 }
             }
             lmax = warp_max(lmax);
-            if (lane == 0) sm.wmax[((step + 1) & 1) * 32 + warp] = lmax;
+            if (lane == 0) sm.wmax[((step + 1) & 1) * 32 + warp] = (double)lmax;
         }
         __syncthreads();
         if (pdf_post && pend) pdf_row(a, sm.gbuf, gi, b, pend_n, tid, T);
@@ -559,12 +589,12 @@ __global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
     // loop ran N B2 phases (steps 0..N-1), so its wz parity is (N-1) & 1.
     const int lastpar = (N - 1) & 1;
     if (want_post && pend) {
-        float Z = block_lse_from(sm.wz + lastpar * 64, W, lane);
+        V Z = block_lse_from<V>(sm.wz + lastpar * 64, W, lane);
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             int j = tid + k * T;
             if (j >= K) continue;
-            float gam = (Z == NEG_INF) ? 0.f : ex2(xpost[k] - Z);
+            float gam = (Z == ninf<V>()) ? 0.f : ex2((float)(xpost[k] - Z));
             if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pend_n * K + j] = gam;
             else sm.gbuf[j] = gam;
         }
@@ -573,26 +603,26 @@ __global__ void __launch_bounds__(1024, 1) k_fb(const FBArgs a) {
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
     {
-        float zm = NEG_INF, zs = 0.f;
+        V zm = ninf<V>();
+        float zs = 0.f;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             int j = tid + k * T;
             if (j >= K) continue;
-            float x = ucand[k] + (BWD ? G.init2[s0 + j] : G.final2[s0 + j]);
-            if (x > zm) { zs = (zm == NEG_INF ? 0.f : zs * ex2(zm - x)) + 1.f; zm = x; }
-            else if (x != NEG_INF) zs += ex2(x - zm);
+            lse_push(zm, zs, ucand[k] + (V)(BWD ? G.init2[s0 + j] : G.final2[s0 + j]));
         }
         if (bad) sm.flag[0] = 1;
         warp_lse(zm, zs);
         __syncthreads();  // all readers of wz[lastpar] are done
-        if (lane == 0) { sm.wz[(lastpar ^ 1) * 64 + 2 * warp] = zm; sm.wz[(lastpar ^ 1) * 64 + 2 * warp + 1] = zs; }
+        if (lane == 0) {
+            sm.wz[(lastpar ^ 1) * 64 + 2 * warp] = (double)zm;
+            sm.wz[(lastpar ^ 1) * 64 + 2 * warp + 1] = (double)zs;
+        }
         __syncthreads();
         if (warp == 0) {
-            float m = lane < W ? sm.wz[(lastpar ^ 1) * 64 + 2 * lane] : NEG_INF;
-            float s = lane < W ? sm.wz[(lastpar ^ 1) * 64 + 2 * lane + 1] : 0.f;
-            warp_lse(m, s);
+            V m = block_lse_from<V>(sm.wz + (lastpar ^ 1) * 64, W, lane);
             if (lane == 0) {
-                double z = (m == NEG_INF) ? -INFINITY : (scale + (double)m + (double)log2f(s)) * kLN2;
+                double z = (m == ninf<V>()) ? -INFINITY : (scale + (double)m) * kLN2;
                 int stt = st;
                 if (sm.flag[0]) stt |= FB_SEQ_NONFINITE_INPUT;
                 if (!(z > -INFINITY)) stt |= FB_SEQ_EMPTY_LATTICE;
@@ -612,7 +642,7 @@ __global__ void __launch_bounds__(256) k_posteriors(const Graph G, const float *
                                                     int D, int pdf_level, float *post) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float *g = (float *)smem_raw;  // K_max
-    __shared__ float wz[2 * 32];
+    __shared__ double wz[2 * 32];
     const int row = blockIdx.x;
     const int b = row / N_max, n = row % N_max;
     const int gi = (G.G == 1) ? 0 : b;
@@ -630,13 +660,12 @@ __global__ void __launch_bounds__(256) k_posteriors(const Graph G, const float *
     for (int j = tid; j < K; j += blockDim.x) {
         float x = (__ldg(alpha + base + j) + __ldg(beta + base + j)) * kL2E;
         g[j] = x;
-        if (x > zm) { zs = (zm == NEG_INF ? 0.f : zs * ex2(zm - x)) + 1.f; zm = x; }
-        else if (x != NEG_INF) zs += ex2(x - zm);
+        lse_push(zm, zs, x);
     }
     warp_lse(zm, zs);
     if (lane == 0) { wz[2 * warp] = zm; wz[2 * warp + 1] = zs; }
     __syncthreads();
-    float Z = block_lse_from(wz, W, lane);
+    float Z = block_lse_from<float>(wz, W, lane);
     for (int j = tid; j < K; j += blockDim.x) {
         float gam = (Z == NEG_INF) ? 0.f : ex2(g[j] - Z);
         if (pdf_level) g[j] = gam;
@@ -696,19 +725,25 @@ __global__ void k_totals(const double *zn, const double *zd, const int *lengths,
 
 using KFn = void (*)(FBArgs);
 
-template <bool BWD, int MODE>
+template <bool BWD, int MODE, int MAXT>
 static KFn pick_spt(int spt) {
     switch (spt) {
-        case 1: return k_fb<BWD, MODE, 1>;
-        case 2: return k_fb<BWD, MODE, 2>;
-        case 4: return k_fb<BWD, MODE, 4>;
-        default: return k_fb<BWD, MODE, 8>;
+        case 1: return k_fb<BWD, MODE, 1, MAXT>;
+        case 2: return k_fb<BWD, MODE, 2, MAXT>;
+        case 4: return k_fb<BWD, MODE, 4, MAXT>;
+        default: return k_fb<BWD, MODE, 8, MAXT>;
     }
 }
 
-static KFn pick(bool bwd, int mode, int spt) {
-    if (bwd) return mode == MODE_FACTORED ? pick_spt<true, MODE_FACTORED>(spt) : pick_spt<true, MODE_EXACT>(spt);
-    return mode == MODE_FACTORED ? pick_spt<false, MODE_FACTORED>(spt) : pick_spt<false, MODE_EXACT>(spt);
+// MAXT = 256 variants (≤ 128 registers, two CTAs per SM) for small CTAs; 1024 otherwise.
+template <bool BWD, int MODE>
+static KFn pick_t(int spt, int T) {
+    return T <= 256 ? pick_spt<BWD, MODE, 256>(spt) : pick_spt<BWD, MODE, 1024>(spt);
+}
+
+static KFn pick(bool bwd, int mode, int spt, int T) {
+    if (bwd) return mode == MODE_FACTORED ? pick_t<true, MODE_FACTORED>(spt, T) : pick_t<true, MODE_EXACT>(spt, T);
+    return mode == MODE_FACTORED ? pick_t<false, MODE_FACTORED>(spt, T) : pick_t<false, MODE_EXACT>(spt, T);
 }
 
 static fb_status check_launch(const char *what) {
@@ -721,7 +756,7 @@ static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s) {
     const Graph &G = a.g;
     const bool post = bwd && a.post_kind != POST_NONE;
     size_t sm = smem_bytes(G, bwd, post);
-    KFn fn = pick(bwd, G.mode, G.spt);
+    KFn fn = pick(bwd, G.mode, G.spt, G.T);
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
     {
@@ -862,7 +897,13 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     cudaStream_t s = (cudaStream_t)stream;
     SideRes *sr = side_res();
     fb_status r;
-    // numerator pass on the side stream (runs on the SMs the B denominator CTAs leave idle)
+    // denominator forward first: its B CTAs each take a whole SM (registers and
+    // shared memory), so the numerator CTAs forked next land on the idle SMs.
+    {
+        FBArgs a = base_args(den, log_emis, lengths, B, N_max);
+        a.lat = den_alpha; a.logZ = zd; a.status = seq_status;
+        if ((r = launch_fb(false, a, s)) != FB_OK) return r;
+    }
     cudaEventRecord(sr->fork, s);
     cudaStreamWaitEvent(sr->s, sr->fork, 0);
     {
@@ -874,12 +915,6 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
         if ((r = launch_fb(true, c, sr->s)) != FB_OK) return r;
     }
     cudaEventRecord(sr->join, sr->s);
-    // denominator forward on the caller's stream, concurrently
-    {
-        FBArgs a = base_args(den, log_emis, lengths, B, N_max);
-        a.lat = den_alpha; a.logZ = zd; a.status = seq_status;
-        if ((r = launch_fb(false, a, s)) != FB_OK) return r;
-    }
     cudaStreamWaitEvent(s, sr->join, 0);
     // denominator backward + fused posterior/gradient epilogue + loss
     {
