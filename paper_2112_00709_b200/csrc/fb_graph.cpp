@@ -36,7 +36,7 @@ namespace {
 
 struct HostSched {
     std::vector<uint2> rec;
-    std::vector<int> rec_rows, warp_row, warp_nslot, lane_cnt, segptr, nseg;
+    std::vector<int> rec_rows, warp_row, warp_nsl, warp_sl0, sl_off, sl_len, sl_seg, segptr, nseg;
     std::vector<long long> rec_off;
     int rows_max = 0, nseg_max = 0, slots_max = 0;
 };
@@ -48,59 +48,66 @@ struct RowLists {
     std::vector<double> w;  // natural log
 };
 
-// Per-thread nnz-balanced schedule for one member (appends to hs).
-bool build_member_sched(const RowLists &rl, int K, int T, int mode, HostSched &hs) {
+// Sliced-ELL schedule for one member graph (appends to hs); see Sched.
+// esize = bytes per element of the gathered u / p arrays.
+bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, HostSched &hs) {
     const int W = T / 32;
     const long long nnz = rl.ptr[K];
-    const long long L = std::max<long long>(1, (nnz + T - 1) / T);
-    // segments in row order
-    std::vector<int> seg_row, seg_begin, seg_len;
+    // per-warp row budget P; segments ≤ Lmax ≈ P/3 so LPT balances warps to ~1/3 of a slice
+    const long long P = std::max<long long>(1, (nnz + 32LL * W - 1) / (32LL * W));
+    const long long Lmax = std::max<long long>(4, P / 3);
+    std::vector<int> seg_begin, seg_len;
     std::vector<int> segptr(K + 1, 0);
     for (int r = 0; r < K; ++r) {
-        segptr[r] = (int)seg_row.size();
+        segptr[r] = (int)seg_len.size();
         long long deg = rl.ptr[r + 1] - rl.ptr[r];
         if (deg == 0) continue;
-        long long ns = (deg + L - 1) / L;
+        long long ns = (deg + Lmax - 1) / Lmax;
         long long base = deg / ns, rem = deg % ns, b = rl.ptr[r];
         for (long long s = 0; s < ns; ++s) {
             long long len = base + (s < rem ? 1 : 0);
-            seg_row.push_back(r);
             seg_begin.push_back((int)b);
             seg_len.push_back((int)len);
             b += len;
         }
     }
-    segptr[K] = (int)seg_row.size();
-    const int nseg = (int)seg_row.size();
-    if (nseg > 65535 || K > 65536) return false;
-    // LPT: longest segment first onto the least-loaded thread (ties → lowest id)
+    segptr[K] = (int)seg_len.size();
+    const int nseg = (int)seg_len.size();
+    if (nseg > 65535 || (long long)K * esize > (1LL << 31)) return false;  // seg ids are packed in 16 bits
+    // slices: segments sorted by length (desc, then id), 32 per slice
     std::vector<int> order(nseg);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return seg_len[a] > seg_len[b]; });
+    const int nsl = (nseg + 31) / 32;
+    std::vector<int> slen(nsl, 0);
+    for (int q = 0; q < nsl; ++q) slen[q] = seg_len[order[32 * q]];
+    // LPT: slices (already longest first) onto the least-loaded warp
     using Item = std::pair<long long, int>;
     std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
-    for (int t = 0; t < T; ++t) heap.push({0, t});
-    std::vector<std::vector<int>> tsegs(T);
-    for (int s : order) {
+    for (int w = 0; w < W; ++w) heap.push({0, w});
+    std::vector<std::vector<int>> wsl(W);
+    for (int q = 0; q < nsl; ++q) {
         Item it = heap.top();
         heap.pop();
-        tsegs[it.second].push_back(s);
-        heap.push({it.first + seg_len[s], it.second});
+        wsl[it.second].push_back(q);
+        heap.push({it.first + slen[q], it.second});
     }
-    std::vector<int> lane_cnt(T, 0);
-    for (int t = 0; t < T; ++t) {
-        std::sort(tsegs[t].begin(), tsegs[t].end());
-        for (int s : tsegs[t]) lane_cnt[t] += seg_len[s];
-    }
-    std::vector<int> warp_row(W), warp_nslot(W);
-    int rows = 0, slots_max = 0;
+    // layout: warps in order, each warp's slices in order
+    const int sl_base = (int)hs.sl_len.size();
+    std::vector<int> warp_row(W), warp_nsl(W), warp_sl0(W);
+    int rows = 0, nsl_out = 0, slots_max = 0;
+    std::vector<int> new_index(nsl);
     for (int w = 0; w < W; ++w) {
-        int mx = 0;
-        for (int l = 0; l < 32; ++l) mx = std::max(mx, lane_cnt[w * 32 + l]);
         warp_row[w] = rows;
-        warp_nslot[w] = mx;
-        rows += mx;
-        slots_max = std::max(slots_max, mx);
+        warp_sl0[w] = nsl_out;
+        warp_nsl[w] = (int)wsl[w].size();
+        int wr = 0;
+        for (int q : wsl[w]) {
+            new_index[q] = nsl_out++;
+            wr += slen[q];
+        }
+        rows += wr;
+        slots_max = std::max(slots_max, wr);
     }
     const long long off = (long long)hs.rec.size();
     uint2 pad;
@@ -108,28 +115,38 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, HostSched &h
     float padw = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
     std::memcpy(&pad.y, &padw, 4);
     hs.rec.resize(off + (long long)rows * 32, pad);
-    for (int t = 0; t < T; ++t) {
-        int w = t / 32, l = t % 32, slot = 0;
-        for (int s : tsegs[t]) {
-            for (int q = 0; q < seg_len[s]; ++q) {
-                int a = seg_begin[s] + q;
-                uint2 r;
-                r.x = (uint32_t)rl.other[a] & 0xFFFFu;
-                if (q == seg_len[s] - 1) r.x |= (uint32_t)(s + 1) << 16;
-                double wn = rl.w[a];
-                float wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
-                if (std::isinf(wn) && wn < 0) wf = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
-                std::memcpy(&r.y, &wf, 4);
-                hs.rec[off + ((long long)warp_row[w] + slot) * 32 + l] = r;
-                ++slot;
+    hs.sl_len.resize(sl_base + nsl, 0);
+    hs.sl_seg.resize((size_t)(sl_base + nsl) * 32, -1);
+    for (int w = 0; w < W; ++w) {
+        int row = warp_row[w];
+        for (int q : wsl[w]) {
+            int qi = new_index[q];
+            hs.sl_len[sl_base + qi] = slen[q];
+            for (int l = 0; l < 32; ++l) {
+                int x = 32 * q + l;
+                if (x >= nseg) continue;
+                int sgi = order[x];
+                hs.sl_seg[(size_t)(sl_base + qi) * 32 + l] = sgi;
+                for (int t = 0; t < seg_len[sgi]; ++t) {
+                    int a = seg_begin[sgi] + t;
+                    uint2 r;
+                    r.x = (uint32_t)rl.other[a] * (uint32_t)esize;
+                    double wn = rl.w[a];
+                    float wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
+                    if (std::isinf(wn) && wn < 0) wf = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
+                    std::memcpy(&r.y, &wf, 4);
+                    hs.rec[off + ((long long)row + t) * 32 + l] = r;
+                }
             }
+            row += slen[q];
         }
     }
     hs.rec_off.push_back(off);
     hs.rec_rows.push_back(rows);
+    hs.sl_off.push_back(sl_base);
     hs.warp_row.insert(hs.warp_row.end(), warp_row.begin(), warp_row.end());
-    hs.warp_nslot.insert(hs.warp_nslot.end(), warp_nslot.begin(), warp_nslot.end());
-    hs.lane_cnt.insert(hs.lane_cnt.end(), lane_cnt.begin(), lane_cnt.end());
+    hs.warp_nsl.insert(hs.warp_nsl.end(), warp_nsl.begin(), warp_nsl.end());
+    hs.warp_sl0.insert(hs.warp_sl0.end(), warp_sl0.begin(), warp_sl0.end());
     hs.segptr.insert(hs.segptr.end(), segptr.begin(), segptr.end());
     hs.nseg.push_back(nseg);
     hs.rows_max = std::max(hs.rows_max, rows);
@@ -162,17 +179,8 @@ bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
 }  // namespace
 
 size_t smem_bytes(const Graph &g, bool backward, bool post) {
-    // must match carve<V>() in fb_kernels.cu; V = double in exact mode
     const Sched &s = backward ? g.bwd : g.fwd;
-    const size_t vsz = g.mode == MODE_EXACT ? 8 : 4;
-    size_t b = 0;
-    b += align16((size_t)s.rows_max * 32 * 8);                        // arc records
-    b += align16((size_t)g.K_max * vsz);                              // u (log2 domain)
-    if (g.mode == MODE_FACTORED) b += align16((size_t)g.K_max * 4);   // p = exp2(u)
-    b += align16((size_t)std::max(1, s.nseg_max) * vsz);              // segment partials
-    if (backward && post) b += align16((size_t)g.K_max * 4);          // γ row for the pdf gather
-    b += align16(8 * (2 * 32 + 2 * 64) + 64);                         // reductions + flags
-    return b;
+    return smem_layout(s.rows_max, g.K_max, s.nseg_max, g.mode == MODE_EXACT, backward && post).total;
 }
 
 }  // namespace fbx
@@ -250,8 +258,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     else
         T = std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 3) / 4)));
     T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
-    int spt = pow2ceil((gr.K_max + T - 1) / T);
-    if (spt > kMaxSPT) return FB_ERR_UNSUPPORTED;
+    int spt = (gr.K_max + T - 1) / T;
+    spt = spt <= 4 ? spt : (spt <= 6 ? 6 : 8);  // instantiated: 1, 2, 3, 4, 6, 8
+    if ((gr.K_max + T - 1) / T > kMaxSPT) return FB_ERR_UNSUPPORTED;
     gr.T = T;
     gr.W = T / 32;
     gr.spt = spt;
@@ -296,8 +305,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
                 in.other[p] = i;
                 in.w[p] = outl.w[a];
             }
-        if (!build_member_sched(in, K, T, gr.mode, hf)) return FB_ERR_UNSUPPORTED;
-        if (!build_member_sched(outl, K, T, gr.mode, hb)) return FB_ERR_UNSUPPORTED;
+        const int esize = gr.mode == MODE_EXACT ? 8 : 4;
+        if (!build_member_sched(in, K, T, gr.mode, esize, hf)) return FB_ERR_UNSUPPORTED;
+        if (!build_member_sched(outl, K, T, gr.mode, esize, hb)) return FB_ERR_UNSUPPORTED;
         // BFS over finite arcs: distance to a final state (reverse) / from an initial state
         std::deque<int> q;
         for (int k = 0; k < K; ++k)
@@ -338,6 +348,17 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         gr.pm.U_max = std::max(gr.pm.U_max, local);
     }
     gr.pm.U_tot = slot_off[G];
+    for (int i = 0; i < K_tot; ++i) {
+        if (dist_fin[i] > 0) gr.mask_fwd = 1;
+        if (dist_start[i] > 0) gr.mask_bwd = 1;
+    }
+    // records address the gathered array directly: byte offset from the start of
+    // dynamic shared memory (p in factored mode, u in exact mode)
+    for (HostSched *h : {&hf, &hb}) {
+        SmemLayout L = smem_layout(h->rows_max, gr.K_max, h->nseg_max, gr.mode == MODE_EXACT, false);
+        const uint32_t base = (uint32_t)(gr.mode == MODE_EXACT ? L.u : L.p);
+        for (auto &r : h->rec) r.x += base;
+    }
     gr.fwd.rows_max = hf.rows_max; gr.fwd.nseg_max = hf.nseg_max; gr.fwd.slots_max = hf.slots_max;
     gr.bwd.rows_max = hb.rows_max; gr.bwd.nseg_max = hb.nseg_max; gr.bwd.slots_max = hb.slots_max;
     if (smem_bytes(gr, false, false) > (size_t)kSmemLimit || smem_bytes(gr, true, true) > (size_t)kSmemLimit)
@@ -348,12 +369,15 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     std::vector<int> soff(state_offsets, state_offsets + G + 1);
     size_t o_soff = pk.put(soff), o_pdf = pk.put(pdf), o_i2 = pk.put(init2), o_f2 = pk.put(final2);
     size_t o_df = pk.put(dist_fin), o_ds = pk.put(dist_start);
-    size_t o_frec = pk.put(hf.rec), o_frr = pk.put(hf.rec_rows), o_fro = pk.put(hf.rec_off),
-           o_fwr = pk.put(hf.warp_row), o_fwn = pk.put(hf.warp_nslot), o_flc = pk.put(hf.lane_cnt),
-           o_fsp = pk.put(hf.segptr), o_fns = pk.put(hf.nseg);
-    size_t o_brec = pk.put(hb.rec), o_brr = pk.put(hb.rec_rows), o_bro = pk.put(hb.rec_off),
-           o_bwr = pk.put(hb.warp_row), o_bwn = pk.put(hb.warp_nslot), o_blc = pk.put(hb.lane_cnt),
-           o_bsp = pk.put(hb.segptr), o_bns = pk.put(hb.nseg);
+    struct SO { size_t rec, rr, ro, wr, wn, w0, so, sl, ss, sp, ns; };
+    auto put_sched = [&](HostSched &h) {
+        SO o;
+        o.rec = pk.put(h.rec); o.rr = pk.put(h.rec_rows); o.ro = pk.put(h.rec_off); o.wr = pk.put(h.warp_row);
+        o.wn = pk.put(h.warp_nsl); o.w0 = pk.put(h.warp_sl0); o.so = pk.put(h.sl_off); o.sl = pk.put(h.sl_len);
+        o.ss = pk.put(h.sl_seg); o.sp = pk.put(h.segptr); o.ns = pk.put(h.nseg);
+        return o;
+    };
+    SO of = put_sched(hf), ob = put_sched(hb);
     size_t o_so = pk.put(slot_off), o_spd = pk.put(slot_pdf), o_ssp = pk.put(slot_sptr),
            o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot);
     void *dev = nullptr;
@@ -371,14 +395,14 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.final2 = (const float *)P(o_f2);
     gr.dist_fin = (const int *)P(o_df);
     gr.dist_start = (const int *)P(o_ds);
-    gr.fwd.rec = (const uint2 *)P(o_frec); gr.fwd.rec_rows = (const int *)P(o_frr);
-    gr.fwd.rec_off = (const long long *)P(o_fro); gr.fwd.warp_row = (const int *)P(o_fwr);
-    gr.fwd.warp_nslot = (const int *)P(o_fwn); gr.fwd.lane_cnt = (const int *)P(o_flc);
-    gr.fwd.segptr = (const int *)P(o_fsp); gr.fwd.nseg = (const int *)P(o_fns);
-    gr.bwd.rec = (const uint2 *)P(o_brec); gr.bwd.rec_rows = (const int *)P(o_brr);
-    gr.bwd.rec_off = (const long long *)P(o_bro); gr.bwd.warp_row = (const int *)P(o_bwr);
-    gr.bwd.warp_nslot = (const int *)P(o_bwn); gr.bwd.lane_cnt = (const int *)P(o_blc);
-    gr.bwd.segptr = (const int *)P(o_bsp); gr.bwd.nseg = (const int *)P(o_bns);
+    auto set_sched = [&](Sched &d, const SO &o) {
+        d.rec = (const uint2 *)P(o.rec); d.rec_rows = (const int *)P(o.rr); d.rec_off = (const long long *)P(o.ro);
+        d.warp_row = (const int *)P(o.wr); d.warp_nsl = (const int *)P(o.wn); d.warp_sl0 = (const int *)P(o.w0);
+        d.sl_off = (const int *)P(o.so); d.sl_len = (const int *)P(o.sl); d.sl_seg = (const int *)P(o.ss);
+        d.segptr = (const int *)P(o.sp); d.nseg = (const int *)P(o.ns);
+    };
+    set_sched(gr.fwd, of);
+    set_sched(gr.bwd, ob);
     gr.pm.slot_off = (const int *)P(o_so); gr.pm.slot_pdf = (const int *)P(o_spd);
     gr.pm.slot_sptr = (const int *)P(o_ssp); gr.pm.slot_states = (const int *)P(o_sst);
     gr.pm.pdf_slot = (const int *)P(o_pds);

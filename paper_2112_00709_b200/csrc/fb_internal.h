@@ -16,24 +16,34 @@ constexpr int kSmemLimit = 227 * 1024;
 
 enum Mode : int { MODE_FACTORED = 0, MODE_EXACT = 1 };
 
-// One direction's per-thread arc schedule (forward = in-arcs / CSC, backward =
-// out-arcs / CSR).  Records are {meta, w}: meta = other-endpoint (16 bits) |
-// (segment id + 1) << 16 on the last arc of a segment; w = e^{T} (factored) or
-// T·log2(e) (exact).  Member g's records start at rec_off[g] (units of 32-record
-// rows); warp w's slots start at row warp_row[g*W + w] (relative), it has
-// warp_nslot[g*W + w] slots, and lane t has lane_cnt[g*T + t] real records.
+// One direction's arc schedule in sliced-ELL form (forward = in-arcs / CSC of
+// T, backward = out-arcs / CSR; ledger L3).  Rows are cut into segments of at
+// most Lmax arcs; segments sorted by length are grouped 32 at a time into
+// slices (one segment per lane, shorter ones padded with null arcs); slices
+// are packed onto the W warps longest-first.  Every lane of a warp therefore
+// executes the same number of slots with no per-arc control flow.
+//   rec[r*32 + lane] = {byte offset of the other endpoint in the u / p arrays,
+//                       weight: e^{T} (factored) or T·log2(e) (exact)}
+//   member g: records start at rec_off[g]; warp w's slices are
+//   sl_off[g] + warp_sl0[g*W+w] … + warp_nsl[g*W+w], its rows start at
+//   warp_row[g*W+w]; slice q has sl_len[q] rows and lane l reduces into
+//   segment sl_seg[q*32+l] (-1: idle lane).  Segments are numbered in row
+//   order, so state j's segments are [segptr[j], segptr[j+1]).
 struct Sched {
     const uint2 *rec = nullptr;
-    const int *rec_rows = nullptr;   // [G] rows (of 32 records) of member g
-    const long long *rec_off = nullptr; // [G] first record of member g
-    const int *warp_row = nullptr;   // [G*W]
-    const int *warp_nslot = nullptr; // [G*W]
-    const int *lane_cnt = nullptr;   // [G*T]
-    const int *segptr = nullptr;     // member g at state_off[g] + g, K_g + 1 entries
-    const int *nseg = nullptr;       // [G]
-    int rows_max = 0;                // max rec_rows
+    const int *rec_rows = nullptr;      // [G]
+    const long long *rec_off = nullptr; // [G]
+    const int *warp_row = nullptr;      // [G*W]
+    const int *warp_nsl = nullptr;      // [G*W]
+    const int *warp_sl0 = nullptr;      // [G*W]
+    const int *sl_off = nullptr;        // [G]
+    const int *sl_len = nullptr;        // [Σ slices]
+    const int *sl_seg = nullptr;        // [Σ slices * 32]
+    const int *segptr = nullptr;        // member g at state_off[g] + g, K_g + 1 entries
+    const int *nseg = nullptr;          // [G]
+    int rows_max = 0;                   // max rec_rows
     int nseg_max = 0;
-    int slots_max = 0;
+    int slots_max = 0;                  // max rows of one warp
 };
 
 // Inverse pdf map of each member: slots = distinct pdfs used by the graph, in
@@ -52,6 +62,7 @@ struct PdfMap {
 
 struct Graph {
     int G = 0, K_tot = 0, D = 0, T = 0, W = 0, spt = 1, mode = 0;
+    int mask_fwd = 0, mask_bwd = 0;  // any state ever masked by the viability distances
     long long nnz = 0;
     int K_max = 0;
     long long nnz_max = 0;
@@ -68,6 +79,33 @@ struct Graph {
     size_t block_bytes = 0;
     int device = 0;
 };
+
+#ifdef __CUDACC__
+#define FBX_HD __host__ __device__
+#else
+#define FBX_HD
+#endif
+
+// Shared-memory carve-up of one forward/backward CTA (host and device agree):
+// arc records | u (log2 values, V) | p = 2^u (factored) | segment partials (V)
+// | γ row (pdf-level epilogue) | reductions + flags.
+struct SmemLayout {
+    size_t rec, u, p, part, gbuf, red, total;
+};
+FBX_HD inline size_t fbx_a16(size_t x) { return (x + 15) & ~size_t(15); }
+FBX_HD inline SmemLayout smem_layout(int rows_max, int K_max, int nseg_max, bool exact, bool gbuf) {
+    const size_t vsz = exact ? 8 : 4;
+    SmemLayout L;
+    size_t o = 0;
+    L.rec = o; o += fbx_a16((size_t)rows_max * 32 * 8);
+    L.u = o; o += fbx_a16((size_t)K_max * vsz);
+    L.p = o; if (!exact) o += fbx_a16((size_t)K_max * 4);
+    L.part = o; o += fbx_a16((size_t)(nseg_max > 0 ? nseg_max : 1) * vsz);
+    L.gbuf = o; if (gbuf) o += fbx_a16((size_t)K_max * 4);
+    L.red = o; o += fbx_a16(8 * (2 * 32 + 2 * 64) + 64);
+    L.total = o;
+    return L;
+}
 
 // Dynamic shared memory needed by a forward/backward launch over this graph.
 size_t smem_bytes(const Graph &g, bool backward, bool pdf_level);

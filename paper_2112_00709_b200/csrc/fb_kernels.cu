@@ -144,13 +144,13 @@ __device__ __forceinline__ void warp_lse(V &m, float &s) {
 }
 __device__ __forceinline__ size_t align16d(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Online max-then-sum over one segment, re-reading its records (fallback path
-// of factored mode, where weights are stored as e^{T}).  Accurate libm ops.
-__device__ __noinline__ float exact_segment(const uint2 *col, int s_begin, int s_end, const float *u) {
+// Online max-then-sum over one segment column of L records (fallback path of
+// factored mode, where weights are stored as e^{T}).  Accurate libm ops.
+__device__ __noinline__ float exact_segment(const uint2 *col, int L, const unsigned char *smem, unsigned p_minus_u) {
     float m = NEG_INF, sum = 0.f;
-    for (int s = s_begin; s <= s_end; ++s) {
+    for (int s = 0; s < L; ++s) {
         uint2 r = col[s * 32];
-        float x = u[r.x & 0xFFFFu] + log2f(__uint_as_float(r.y));
+        float x = *(const float *)(smem + (r.x - p_minus_u)) + log2f(__uint_as_float(r.y));
         if (x == NEG_INF) continue;
         if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
         else sum += exp2f(x - m);
@@ -197,16 +197,14 @@ struct Smem {
 template <class V>
 __device__ __forceinline__ Smem<V> carve(unsigned char *base, const Graph &G, bool bwd, bool post, int mode) {
     const Sched &S = bwd ? G.bwd : G.fwd;
+    SmemLayout L = smem_layout(S.rows_max, G.K_max, S.nseg_max, mode == MODE_EXACT, bwd && post);
     Smem<V> m;
-    size_t off = 0;
-    m.rec = (uint2 *)(base + off); off += align16d((size_t)S.rows_max * 32 * 8);
-    m.u = (V *)(base + off); off += align16d((size_t)G.K_max * sizeof(V));
-    m.p = nullptr;
-    if (mode == MODE_FACTORED) { m.p = (float *)(base + off); off += align16d((size_t)G.K_max * 4); }
-    m.part = (V *)(base + off); off += align16d((size_t)max(1, S.nseg_max) * sizeof(V));
-    m.gbuf = nullptr;
-    if (bwd && post) { m.gbuf = (float *)(base + off); off += align16d((size_t)G.K_max * 4); }
-    m.wmax = (double *)(base + off);
+    m.rec = (uint2 *)(base + L.rec);
+    m.u = (V *)(base + L.u);
+    m.p = mode == MODE_FACTORED ? (float *)(base + L.p) : nullptr;
+    m.part = (V *)(base + L.part);
+    m.gbuf = (bwd && post) ? (float *)(base + L.gbuf) : nullptr;
+    m.wmax = (double *)(base + L.red);
     m.wz = m.wmax + 64;
     m.flag = (int *)(m.wz + 128);
     return m;
@@ -241,66 +239,61 @@ __device__ __forceinline__ V combine_segments(const V *part, int packed) {
     return m + (V)lg2(s);
 }
 
-// Phase A: reduce this lane's slot column into the segment partials.
-//  factored: Σ p_src · e^{T} (one FMA per arc), exact fallback outside [2^-80, 2^120];
-//  exact:    online max-then-sum in V (double for exact mode) with one ex2 per arc.
+// Phase A: walk this warp's slices; lane l reduces one row segment per slice.
+//  factored: Σ p_src · e^{T} (one FMA per arc, two accumulators), exact
+//            fallback when the sum leaves [2^-80, 2^120];
+//  exact:    online max-then-sum in V (double) with one ex2 per arc (two chains).
 template <int MODE, class V>
-__device__ __forceinline__ void phase_a(const uint2 *col, int cnt, const V *u, const float *p, V *part) {
+__device__ __forceinline__ void phase_a(const uint2 *col, const int *slen, const int *sseg, int nsl,
+                                        const unsigned char *smem, unsigned p_minus_u, V *part) {
     constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
     constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
-    if (MODE == MODE_FACTORED) {
-        int seg_start = 0;
-        float acc = 0.f;
-        for (int s = 0; s < cnt; s += 4) {
-            uint2 r[4];
-            float pv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) r[q] = (s + q < cnt) ? col[(s + q) * 32] : make_uint2(0u, 0u);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) pv[q] = p[r[q].x & 0xFFFFu];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (s + q < cnt) {
-                    acc = fmaf(pv[q], __uint_as_float(r[q].y), acc);
-                    unsigned sg = r[q].x >> 16;
-                    if (sg) {
-                        float val = (acc >= kTiny && acc <= kHuge)
-                                        ? lg2(acc)
-                                        : exact_segment(col, seg_start, s + q, (const float *)u);
-                        part[sg - 1] = (V)val;
-                        acc = 0.f;
-                        seg_start = s + q + 1;
-                    }
-                }
+    // records hold byte offsets from the start of dynamic shared memory
+    const unsigned char *ub = smem;
+    const unsigned char *pb = smem;
+    for (int q = 0; q < nsl; ++q) {
+        const int L = __ldg(slen + q);
+        const int seg = __ldg(sseg + q * 32);
+        if (MODE == MODE_FACTORED) {
+            float a0 = 0.f, a1 = 0.f;
+            int s = 0;
+            for (; s + 4 <= L; s += 4) {
+                uint2 r0 = col[(s + 0) * 32], r1 = col[(s + 1) * 32], r2 = col[(s + 2) * 32], r3 = col[(s + 3) * 32];
+                float p0 = *(const float *)(pb + r0.x), p1 = *(const float *)(pb + r1.x);
+                float p2 = *(const float *)(pb + r2.x), p3 = *(const float *)(pb + r3.x);
+                a0 = fmaf(p0, __uint_as_float(r0.y), a0);
+                a1 = fmaf(p1, __uint_as_float(r1.y), a1);
+                a0 = fmaf(p2, __uint_as_float(r2.y), a0);
+                a1 = fmaf(p3, __uint_as_float(r3.y), a1);
             }
-        }
-    } else {
-        V m = ninf<V>();
-        float sum = 0.f;
-        for (int s = 0; s < cnt; s += 4) {
-            uint2 r[4];
-            V uv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) r[q] = (s + q < cnt) ? col[(s + q) * 32] : make_uint2(0u, 0u);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) uv[q] = u[r[q].x & 0xFFFFu];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (s + q < cnt) {
-                    V x = uv[q] + (V)__uint_as_float(r[q].y);
-                    V hi = vmax(m, x), lo = vmin(m, x);
-                    float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
-                    sum = (x > m) ? fmaf(sum, e, 1.f) : sum + e;
-                    m = hi;
-                    unsigned sg = r[q].x >> 16;
-                    if (sg) {
-                        part[sg - 1] = (m == ninf<V>()) ? m : m + (V)lg2(sum);
-                        m = ninf<V>();
-                        sum = 0.f;
-                    }
-                }
+            for (; s < L; ++s) {
+                uint2 r = col[s * 32];
+                a0 = fmaf(*(const float *)(pb + r.x), __uint_as_float(r.y), a0);
             }
+            float acc = a0 + a1;
+            if (seg >= 0)
+                part[seg] = (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_segment(col, L, smem, p_minus_u));
+        } else {
+            V m0 = ninf<V>(), m1 = ninf<V>();
+            float s0 = 0.f, s1 = 0.f;
+            int s = 0;
+            auto push = [&](V &m, float &sm, uint2 r) {
+                V x = *(const V *)(ub + r.x) + (V)__uint_as_float(r.y);
+                V hi = vmax(m, x), lo = vmin(m, x);
+                float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
+                sm = (x > m) ? fmaf(sm, e, 1.f) : sm + e;
+                m = hi;
+            };
+            for (; s + 2 <= L; s += 2) {
+                uint2 r0 = col[s * 32], r1 = col[(s + 1) * 32];
+                push(m0, s0, r0);
+                push(m1, s1, r1);
+            }
+            if (s < L) push(m0, s0, col[s * 32]);
+            lse_combine(m0, s0, m1, s1);
+            if (seg >= 0) part[seg] = (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0);
         }
+        col += L * 32;
     }
 }
 
@@ -385,6 +378,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     Smem<V> sm = carve<V>(smem_raw, G, BWD, want_post, MODE);
     const V L2E = (V)1.4426950408889634;
     const V LN2 = (V)0.6931471805599453;
+    const V NINF = ninf<V>();
 
     int st = 0;
     if (BWD) {
@@ -411,50 +405,49 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         for (int x = tid; x < n16; x += T) dst[x] = src[x];
     }
     if (tid == 0) sm.flag[0] = 0;
-    const int wrow = S.warp_row[gi * W + warp];
-    const int mycnt = S.lane_cnt[gi * T + tid];
-    const uint2 *mycol = sm.rec + (size_t)wrow * 32 + lane;
+    const int wsl0 = S.sl_off[gi] + S.warp_sl0[gi * W + warp];
+    const int nsl = S.warp_nsl[gi * W + warp];
+    const int *slen = S.sl_len + wsl0;
+    const int *sseg = S.sl_seg + (size_t)wsl0 * 32 + lane;
+    const uint2 *mycol = sm.rec + (size_t)S.warp_row[gi * W + warp] * 32 + lane;
+    const bool use_mask = BWD ? G.mask_bwd : G.mask_fwd;
+    const unsigned p_minus_u = MODE == MODE_FACTORED ? (unsigned)((unsigned char *)sm.p - (unsigned char *)sm.u) : 0u;
 
-    // owned states j = tid + k*T: packed segment range, pdf | viability distance
-    int segp[SPT];
-    unsigned pdfd[SPT];
+    // Owned states j = tid + k*T (k < SPT).  Slots with j ≥ K are inert: no
+    // segments (y = 0̄), pdf 0, never stored.
+    int segp[SPT];      // first segment | count << 16
+    int pdfk[SPT];      // emission column
+    int distk[SPT];     // viability distance
     const int *segptr = S.segptr + s0 + gi;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
         int j = tid + k * T;
+        segp[k] = 0; pdfk[k] = 0; distk[k] = 0;
         if (j < K) {
             int a0 = segptr[j], a1 = segptr[j + 1];
             segp[k] = a0 | ((a1 - a0) << 16);
-            int dist = BWD ? G.dist_start[s0 + j] : G.dist_fin[s0 + j];
-            dist = min(dist, 4095);
-            pdfd[k] = (unsigned)G.pdf[s0 + j] | ((unsigned)dist << 20);
-        } else {
-            segp[k] = 0;
-            pdfd[k] = 4095u << 20;
+            pdfk[k] = G.pdf[s0 + j];
+            distk[k] = BWD ? G.dist_start[s0 + j] : G.dist_fin[s0 + j];
         }
     }
     const float *em = a.emis + (size_t)b * a.N_max * a.D;
     const size_t lat_base = (size_t)a.N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
     auto load_v = [&](int n, float *v) {
+        const float *row = em + (size_t)min(max(n, 0), N - 1) * a.D;
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-            int j = tid + k * T;
-            v[k] = (j < K && n >= 0 && n < N) ? __ldg(em + (size_t)n * a.D + (pdfd[k] & 0xFFFFF)) : 0.f;
-        }
+        for (int k = 0; k < SPT; ++k) v[k] = __ldg(row + pdfk[k]);
     };
     auto load_alpha = [&](int n, float *v) {
+        const float *row = a.alpha + lat_base + (size_t)min(max(n, 0), N - 1) * K;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             int j = tid + k * T;
-            v[k] = (j < K && n >= 0 && n < N) ? __ldg(a.alpha + lat_base + (size_t)n * K + j) : 0.f;
+            v[k] = __ldg(row + min(j, K - 1));
         }
     };
-    // viable(j, n): forward — a final state is reachable in the N-1-n remaining
+    // viable(k, n): forward — a final state is reachable in the N-1-n remaining
     // transitions; backward — the state is reachable from an initial state in n.
-    auto viable = [&](int k, int n) {
-        int dist = (int)(pdfd[k] >> 20);
-        return BWD ? (dist <= n) : (dist <= N - 1 - n);
-    };
+    auto viable = [&](int k, int n) { return !use_mask || (BWD ? (distk[k] <= n) : (distk[k] <= N - 1 - n)); };
 
     float vcur[SPT], vnxt[SPT];   // emissions of the frame being produced and the next one
     float acur[SPT], anxt[SPT];   // α̂ prefetch (backward epilogue)
@@ -466,26 +459,25 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     load_v(n_first + dir, vnxt);
     if (want_post) { load_alpha(n_first, acur); load_alpha(n_first + dir, anxt); }
     double scale = 0.0;   // C_n (fwd) / D_n (bwd), log2 units
-    bool bad = false;
+    float vsum = 0.f;     // Σ of every emission read: NaN / +∞ ⇒ non-finite input
     bool pend = false;    // a posterior row is pending (its Z in wz[parity])
     int pend_n = 0;
-    __syncthreads();  // schedule, flag visible
 
     // ---- frame n_first: π ⊗ v_0 (fwd, L6) / β̂_{N-1} = ω (bwd, L7)
     {
-        V lmax = ninf<V>();
+        V lmax = NINF;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             int j = tid + k * T;
-            if (j >= K) { cand[k] = ninf<V>(); ucand[k] = ninf<V>(); continue; }
+            bool ok = j < K && viable(k, n_first);
             float v = vcur[k];
-            if (!(v < INFINITY)) bad = true;
+            vsum += v;
             V v2 = (V)v * L2E;
             if (!BWD) {
-                cand[k] = viable(k, 0) ? (V)G.init2[s0 + j] + v2 : ninf<V>();
+                cand[k] = ok ? (V)G.init2[s0 + min(j, K - 1)] + v2 : NINF;
                 lmax = vmax(lmax, cand[k]);
             } else {
-                cand[k] = viable(k, N - 1) ? (V)G.final2[s0 + j] : ninf<V>();
+                cand[k] = ok ? (V)G.final2[s0 + min(j, K - 1)] : NINF;
                 ucand[k] = cand[k] + v2;
                 lmax = vmax(lmax, ucand[k]);
             }
@@ -493,34 +485,39 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         lmax = warp_max(lmax);
         if (lane == 0) sm.wmax[warp] = (double)lmax;
     }
-    __syncthreads();
+    __syncthreads();  // schedule, wmax visible
     int n = n_first;
     for (int step = 0;; ++step) {
         // ---- phase B2 of frame n: normalise, store, refresh u/p
         {
             V c = block_max_from<V>(sm.wmax + (step & 1) * 32, W, lane);
-            if (c == ninf<V>()) c = (V)0;  // no viable state: keep 0̄ everywhere
+            if (c == NINF) c = (V)0;  // no viable state: keep 0̄ everywhere
             scale += (double)c;
             if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
-            V zm = ninf<V>();
-            float zs = 0.f;
+            float *latn = a.lat ? a.lat + lat_base + (size_t)n * K : nullptr;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
                 int j = tid + k * T;
-                if (j >= K) continue;
                 V h = cand[k] - c;   // α̂_n or β̂_n (log2)
                 V uu = BWD ? ucand[k] - c : h;
-                if (a.lat) a.lat[lat_base + (size_t)n * K + j] = (float)(h * LN2);
-                sm.u[j] = uu;
-                if (MODE == MODE_FACTORED) sm.p[j] = ex2((float)uu);
                 ucand[k] = uu;
-                if (want_post) {
-                    V x = (V)acur[k] * L2E + h;
-                    xpost[k] = x;
-                    lse_push(zm, zs, x);
+                if (j < K) {
+                    if (latn) latn[j] = (float)(h * LN2);
+                    sm.u[j] = uu;
+                    if (MODE == MODE_FACTORED) sm.p[j] = ex2((float)uu);
                 }
+                if (want_post) xpost[k] = (V)acur[k] * L2E + h;
             }
             if (want_post) {
+                // block log-sum-exp of x = α̂_n + β̂_n (the per-frame normaliser Z_n)
+                V zm = NINF;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) zm = vmax(zm, (tid + k * T < K) ? xpost[k] : NINF);
+                float zs = 0.f;
+                if (zm != NINF) {
+#pragma unroll
+                    for (int k = 0; k < SPT; ++k) zs += (tid + k * T < K) ? ex2((float)(xpost[k] - zm)) : 0.f;
+                }
                 warp_lse(zm, zs);
                 if (lane == 0) {
                     sm.wz[(step & 1) * 64 + 2 * warp] = (double)zm;
@@ -544,36 +541,35 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         }
         n = n_next;
         // ---- phase A of frame n
-        phase_a<MODE, V>(mycol, mycnt, sm.u, sm.p, sm.part);
+        phase_a<MODE, V>(mycol, slen, sseg, nsl, smem_raw, p_minus_u, sm.part);
         __syncthreads();
         // ---- phase B1 of frame n (+ pending posterior of frame n - dir)
         {
             if (pend) {
                 V Z = block_lse_from<V>(sm.wz + (step & 1) * 64, W, lane);
+                float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pend_n * K : sm.gbuf;
 #pragma unroll
                 for (int k = 0; k < SPT; ++k) {
                     int j = tid + k * T;
-                    if (j >= K) continue;
-                    float gam = (Z == ninf<V>()) ? 0.f : ex2((float)(xpost[k] - Z));
-                    if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pend_n * K + j] = gam;
-                    else sm.gbuf[j] = gam;
+                    float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
+                    if (j < K) prow[j] = gam;
                 }
             }
-            V lmax = ninf<V>();
+            V lmax = NINF;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
-                int j = tid + k * T;
-                if (j >= K) { cand[k] = ninf<V>(); ucand[k] = ninf<V>(); continue; }
-                V y = combine_segments<V>(sm.part, segp[k]);
+                const int ns = segp[k] >> 16;
+                V y = sm.part[segp[k] & 0xFFFF];
+                if (ns > 1) y = combine_segments<V>(sm.part, segp[k]);
+                const bool ok = ns > 0 && viable(k, n);
                 float v = vcur[k];
-                if (!(v < INFINITY)) bad = true;
+                vsum += v;
                 V v2 = (V)v * L2E;
-                bool ok = viable(k, n);
                 if (!BWD) {
-                    cand[k] = ok ? y + v2 : ninf<V>();
+                    cand[k] = ok ? y + v2 : NINF;
                     lmax = vmax(lmax, cand[k]);
                 } else {
-                    cand[k] = ok ? y : ninf<V>();
+                    cand[k] = ok ? y : NINF;
                     ucand[k] = cand[k] + v2;
                     lmax = vmax(lmax, ucand[k]);
                 }
@@ -590,28 +586,26 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     const int lastpar = (N - 1) & 1;
     if (want_post && pend) {
         V Z = block_lse_from<V>(sm.wz + lastpar * 64, W, lane);
+        float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pend_n * K : sm.gbuf;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             int j = tid + k * T;
-            if (j >= K) continue;
-            float gam = (Z == ninf<V>()) ? 0.f : ex2((float)(xpost[k] - Z));
-            if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pend_n * K + j] = gam;
-            else sm.gbuf[j] = gam;
+            float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
+            if (j < K) prow[j] = gam;
         }
         __syncthreads();
         if (pdf_post) pdf_row(a, sm.gbuf, gi, b, pend_n, tid, T);
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
     {
-        V zm = ninf<V>();
+        V zm = NINF;
         float zs = 0.f;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             int j = tid + k * T;
-            if (j >= K) continue;
-            lse_push(zm, zs, ucand[k] + (V)(BWD ? G.init2[s0 + j] : G.final2[s0 + j]));
+            if (j < K) lse_push(zm, zs, ucand[k] + (V)(BWD ? G.init2[s0 + j] : G.final2[s0 + j]));
         }
-        if (bad) sm.flag[0] = 1;
+        if (!(vsum < INFINITY)) sm.flag[0] = 1;
         warp_lse(zm, zs);
         __syncthreads();  // all readers of wz[lastpar] are done
         if (lane == 0) {
@@ -622,9 +616,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         if (warp == 0) {
             V m = block_lse_from<V>(sm.wz + (lastpar ^ 1) * 64, W, lane);
             if (lane == 0) {
-                double z = (m == ninf<V>()) ? -INFINITY : (scale + (double)m) * kLN2;
+                double z = (m == NINF) ? -INFINITY : (scale + (double)m) * kLN2;
                 int stt = st;
-                if (sm.flag[0]) stt |= FB_SEQ_NONFINITE_INPUT;
+                if (sm.flag[0] == 1) stt |= FB_SEQ_NONFINITE_INPUT;
                 if (!(z > -INFINITY)) stt |= FB_SEQ_EMPTY_LATTICE;
                 if (stt) z = -INFINITY;
                 if (a.logZ) a.logZ[b] = z;
@@ -730,7 +724,9 @@ static KFn pick_spt(int spt) {
     switch (spt) {
         case 1: return k_fb<BWD, MODE, 1, MAXT>;
         case 2: return k_fb<BWD, MODE, 2, MAXT>;
+        case 3: return k_fb<BWD, MODE, 3, MAXT>;
         case 4: return k_fb<BWD, MODE, 4, MAXT>;
+        case 6: return k_fb<BWD, MODE, 6, MAXT>;
         default: return k_fb<BWD, MODE, 8, MAXT>;
     }
 }

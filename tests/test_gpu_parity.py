@@ -189,8 +189,8 @@ def test_status_flags(fbx):
 def test_empty_lattice(fbx):
     # numerator needs ≥ L frames; give it fewer
     rng = np.random.Generator(np.random.PCG64(5))
-    g = synth.numerator_graph(rng, 20, 50, "identity")
-    emis = synth.emissions(rng, 2, 30, 50)
+    g = synth.numerator_graph(rng, 20, 300, "identity")
+    emis = synth.emissions(rng, 2, 30, 300)
     lens = np.array([10, 30], np.int32)
     r = run_fb(fbx, synth.compose([g, g]), emis, lens)
     assert r["st_fwd"][0] == fbx.SEQ_EMPTY_LATTICE and r["st_fwd"][1] == 0
