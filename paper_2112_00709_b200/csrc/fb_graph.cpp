@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -36,9 +37,10 @@ namespace {
 
 struct HostSched {
     std::vector<uint2> rec;
-    std::vector<int> rec_rows, warp_row, warp_nsl, warp_sl0, sl_off, sl_len, sl_seg, segptr, nseg;
+    std::vector<char> is_header;  // per row of 32 records (host only)
+    std::vector<int> rec_rows, warp_row, warp_nsl;
     std::vector<long long> rec_off;
-    int rows_max = 0, nseg_max = 0, slots_max = 0;
+    int rows_max = 0, slots_max = 0;
 };
 
 // Arc lists for one member graph in one direction: row r reduces over
@@ -48,64 +50,55 @@ struct RowLists {
     std::vector<double> w;  // natural log
 };
 
-// Sliced-ELL schedule for one member graph (appends to hs); see Sched.
-// esize = bytes per element of the gathered u / p arrays.
-bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, HostSched &hs) {
+// Grouped sliced-ELL schedule for one member graph (appends to hs); see Sched.
+// esize = bytes per element of the gathered u / p arrays; offsets are relative
+// to the gathered array and rebased to shared-memory offsets by the caller.
+bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, int Lmax, HostSched &hs) {
     const int W = T / 32;
-    const long long nnz = rl.ptr[K];
-    // per-warp row budget P; segments ≤ Lmax ≈ P/3 so LPT balances warps to ~1/3 of a slice
-    const long long P = std::max<long long>(1, (nnz + 32LL * W - 1) / (32LL * W));
-    const long long Lmax = std::max<long long>(4, P / 3);
-    std::vector<int> seg_begin, seg_len;
-    std::vector<int> segptr(K + 1, 0);
+    struct RowG { int row, len; };
+    std::vector<RowG> cls[6];  // g = 1, 2, 4, 8, 16, 32
     for (int r = 0; r < K; ++r) {
-        segptr[r] = (int)seg_len.size();
-        long long deg = rl.ptr[r + 1] - rl.ptr[r];
-        if (deg == 0) continue;
-        long long ns = (deg + Lmax - 1) / Lmax;
-        long long base = deg / ns, rem = deg % ns, b = rl.ptr[r];
-        for (long long s = 0; s < ns; ++s) {
-            long long len = base + (s < rem ? 1 : 0);
-            seg_begin.push_back((int)b);
-            seg_len.push_back((int)len);
-            b += len;
+        long long d = rl.ptr[r + 1] - rl.ptr[r];
+        if (d == 0) continue;
+        int lg = 0;
+        while (lg < 5 && (d + (1LL << lg) - 1) / (1LL << lg) > Lmax) ++lg;
+        cls[lg].push_back({r, (int)((d + (1LL << lg) - 1) / (1LL << lg))});
+    }
+    struct Slice { int g, L; std::vector<int> rows; };
+    std::vector<Slice> sl;
+    for (int lg = 0; lg < 6; ++lg) {
+        auto &c = cls[lg];
+        std::stable_sort(c.begin(), c.end(), [](const RowG &a, const RowG &b) { return a.len > b.len; });
+        const int g = 1 << lg, per = 32 / g;
+        for (size_t i = 0; i < c.size(); i += per) {
+            Slice s;
+            s.g = g;
+            s.L = (c[i].len + 3) & ~3;
+            for (size_t t = i; t < std::min(c.size(), i + per); ++t) s.rows.push_back(c[t].row);
+            sl.push_back(std::move(s));
         }
     }
-    segptr[K] = (int)seg_len.size();
-    const int nseg = (int)seg_len.size();
-    if (nseg > 65535 || (long long)K * esize > (1LL << 31)) return false;  // seg ids are packed in 16 bits
-    // slices: segments sorted by length (desc, then id), 32 per slice
-    std::vector<int> order(nseg);
+    // LPT: longest slice first onto the least-loaded warp
+    std::vector<int> order(sl.size());
     std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return seg_len[a] > seg_len[b]; });
-    const int nsl = (nseg + 31) / 32;
-    std::vector<int> slen(nsl, 0);
-    for (int q = 0; q < nsl; ++q) slen[q] = seg_len[order[32 * q]];
-    // LPT: slices (already longest first) onto the least-loaded warp
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sl[a].L > sl[b].L; });
     using Item = std::pair<long long, int>;
     std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
     for (int w = 0; w < W; ++w) heap.push({0, w});
     std::vector<std::vector<int>> wsl(W);
-    for (int q = 0; q < nsl; ++q) {
+    for (int q : order) {
         Item it = heap.top();
         heap.pop();
         wsl[it.second].push_back(q);
-        heap.push({it.first + slen[q], it.second});
+        heap.push({it.first + sl[q].L + 1, it.second});
     }
-    // layout: warps in order, each warp's slices in order
-    const int sl_base = (int)hs.sl_len.size();
-    std::vector<int> warp_row(W), warp_nsl(W), warp_sl0(W);
-    int rows = 0, nsl_out = 0, slots_max = 0;
-    std::vector<int> new_index(nsl);
+    std::vector<int> warp_row(W), warp_nsl(W);
+    int rows = 0, slots_max = 0;
     for (int w = 0; w < W; ++w) {
-        warp_row[w] = rows;
-        warp_sl0[w] = nsl_out;
-        warp_nsl[w] = (int)wsl[w].size();
         int wr = 0;
-        for (int q : wsl[w]) {
-            new_index[q] = nsl_out++;
-            wr += slen[q];
-        }
+        for (int q : wsl[w]) wr += 1 + sl[q].L;
+        warp_row[w] = rows;
+        warp_nsl[w] = (int)wsl[w].size();
         rows += wr;
         slots_max = std::max(slots_max, wr);
     }
@@ -115,44 +108,45 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, H
     float padw = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
     std::memcpy(&pad.y, &padw, 4);
     hs.rec.resize(off + (long long)rows * 32, pad);
-    hs.sl_len.resize(sl_base + nsl, 0);
-    hs.sl_seg.resize((size_t)(sl_base + nsl) * 32, -1);
+    hs.is_header.resize(hs.is_header.size() + rows, 0);
+    const long long hoff = (long long)hs.is_header.size() - rows;
     for (int w = 0; w < W; ++w) {
         int row = warp_row[w];
         for (int q : wsl[w]) {
-            int qi = new_index[q];
-            hs.sl_len[sl_base + qi] = slen[q];
+            const Slice &s = sl[q];
+            hs.is_header[hoff + row] = 1;
             for (int l = 0; l < 32; ++l) {
-                int x = 32 * q + l;
-                if (x >= nseg) continue;
-                int sgi = order[x];
-                hs.sl_seg[(size_t)(sl_base + qi) * 32 + l] = sgi;
-                for (int t = 0; t < seg_len[sgi]; ++t) {
-                    int a = seg_begin[sgi] + t;
-                    uint2 r;
-                    r.x = (uint32_t)rl.other[a] * (uint32_t)esize;
+                int ri = l / s.g, t = l % s.g;
+                bool has = ri < (int)s.rows.size();
+                uint2 h;
+                h.x = (has && t == 0) ? (uint32_t)s.rows[ri] : 0xFFFFFFFFu;
+                h.y = (uint32_t)s.g | ((uint32_t)s.L << 8);
+                hs.rec[off + (long long)row * 32 + l] = h;
+                if (!has) continue;
+                const int r = s.rows[ri];
+                const long long d = rl.ptr[r + 1] - rl.ptr[r];
+                const long long len = (d + s.g - 1) / s.g;
+                const long long a0 = rl.ptr[r] + t * len, a1 = std::min<long long>(rl.ptr[r + 1], a0 + len);
+                for (long long a = a0; a < a1; ++a) {
+                    uint2 rr;
+                    rr.x = (uint32_t)rl.other[a] * (uint32_t)esize;
                     double wn = rl.w[a];
                     float wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
                     if (std::isinf(wn) && wn < 0) wf = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
-                    std::memcpy(&r.y, &wf, 4);
-                    hs.rec[off + ((long long)row + t) * 32 + l] = r;
+                    std::memcpy(&rr.y, &wf, 4);
+                    hs.rec[off + (long long)(row + 1 + (a - a0)) * 32 + l] = rr;
                 }
             }
-            row += slen[q];
+            row += 1 + s.L;
         }
     }
     hs.rec_off.push_back(off);
     hs.rec_rows.push_back(rows);
-    hs.sl_off.push_back(sl_base);
     hs.warp_row.insert(hs.warp_row.end(), warp_row.begin(), warp_row.end());
     hs.warp_nsl.insert(hs.warp_nsl.end(), warp_nsl.begin(), warp_nsl.end());
-    hs.warp_sl0.insert(hs.warp_sl0.end(), warp_sl0.begin(), warp_sl0.end());
-    hs.segptr.insert(hs.segptr.end(), segptr.begin(), segptr.end());
-    hs.nseg.push_back(nseg);
     hs.rows_max = std::max(hs.rows_max, rows);
-    hs.nseg_max = std::max(hs.nseg_max, nseg);
     hs.slots_max = std::max(hs.slots_max, slots_max);
-    return true;
+    return (long long)K * esize < (1LL << 31);
 }
 
 int pow2ceil(long long x) {
@@ -180,7 +174,7 @@ bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
 
 size_t smem_bytes(const Graph &g, bool backward, bool post) {
     const Sched &s = backward ? g.bwd : g.fwd;
-    return smem_layout(s.rows_max, g.K_max, s.nseg_max, g.mode == MODE_EXACT, backward && post).total;
+    return smem_layout(s.rows_max, g.T * g.spt, g.mode == MODE_EXACT, backward && post).total;
 }
 
 }  // namespace fbx
@@ -262,6 +256,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     spt = spt <= 4 ? spt : (spt <= 6 ? 6 : 8);  // instantiated: 1, 2, 3, 4, 6, 8
     if ((gr.K_max + T - 1) / T > kMaxSPT) return FB_ERR_UNSUPPORTED;
     gr.T = T;
+    // longest row segment per lane before a row is split over 2, 4, … lanes
+    int lmax = gr.mode == MODE_FACTORED ? 12 : 4;
+    if (const char *e = std::getenv("FBX_LMAX")) lmax = std::max(1, std::atoi(e));
     gr.W = T / 32;
     gr.spt = spt;
 
@@ -306,8 +303,8 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
                 in.w[p] = outl.w[a];
             }
         const int esize = gr.mode == MODE_EXACT ? 8 : 4;
-        if (!build_member_sched(in, K, T, gr.mode, esize, hf)) return FB_ERR_UNSUPPORTED;
-        if (!build_member_sched(outl, K, T, gr.mode, esize, hb)) return FB_ERR_UNSUPPORTED;
+        if (!build_member_sched(in, K, T, gr.mode, esize, lmax, hf)) return FB_ERR_UNSUPPORTED;
+        if (!build_member_sched(outl, K, T, gr.mode, esize, lmax, hb)) return FB_ERR_UNSUPPORTED;
         // BFS over finite arcs: distance to a final state (reverse) / from an initial state
         std::deque<int> q;
         for (int k = 0; k < K; ++k)
@@ -355,12 +352,14 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     // records address the gathered array directly: byte offset from the start of
     // dynamic shared memory (p in factored mode, u in exact mode)
     for (HostSched *h : {&hf, &hb}) {
-        SmemLayout L = smem_layout(h->rows_max, gr.K_max, h->nseg_max, gr.mode == MODE_EXACT, false);
+        SmemLayout L = smem_layout(h->rows_max, gr.T * gr.spt, gr.mode == MODE_EXACT, false);
         const uint32_t base = (uint32_t)(gr.mode == MODE_EXACT ? L.u : L.p);
-        for (auto &r : h->rec) r.x += base;
+        for (size_t row = 0; row < h->is_header.size(); ++row)
+            if (!h->is_header[row])
+                for (int l = 0; l < 32; ++l) h->rec[row * 32 + l].x += base;
     }
-    gr.fwd.rows_max = hf.rows_max; gr.fwd.nseg_max = hf.nseg_max; gr.fwd.slots_max = hf.slots_max;
-    gr.bwd.rows_max = hb.rows_max; gr.bwd.nseg_max = hb.nseg_max; gr.bwd.slots_max = hb.slots_max;
+    gr.fwd.rows_max = hf.rows_max; gr.fwd.slots_max = hf.slots_max;
+    gr.bwd.rows_max = hb.rows_max; gr.bwd.slots_max = hb.slots_max;
     if (smem_bytes(gr, false, false) > (size_t)kSmemLimit || smem_bytes(gr, true, true) > (size_t)kSmemLimit)
         return FB_ERR_UNSUPPORTED;
 
@@ -369,12 +368,11 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     std::vector<int> soff(state_offsets, state_offsets + G + 1);
     size_t o_soff = pk.put(soff), o_pdf = pk.put(pdf), o_i2 = pk.put(init2), o_f2 = pk.put(final2);
     size_t o_df = pk.put(dist_fin), o_ds = pk.put(dist_start);
-    struct SO { size_t rec, rr, ro, wr, wn, w0, so, sl, ss, sp, ns; };
+    struct SO { size_t rec, rr, ro, wr, wn; };
     auto put_sched = [&](HostSched &h) {
         SO o;
         o.rec = pk.put(h.rec); o.rr = pk.put(h.rec_rows); o.ro = pk.put(h.rec_off); o.wr = pk.put(h.warp_row);
-        o.wn = pk.put(h.warp_nsl); o.w0 = pk.put(h.warp_sl0); o.so = pk.put(h.sl_off); o.sl = pk.put(h.sl_len);
-        o.ss = pk.put(h.sl_seg); o.sp = pk.put(h.segptr); o.ns = pk.put(h.nseg);
+        o.wn = pk.put(h.warp_nsl);
         return o;
     };
     SO of = put_sched(hf), ob = put_sched(hb);
@@ -397,9 +395,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.dist_start = (const int *)P(o_ds);
     auto set_sched = [&](Sched &d, const SO &o) {
         d.rec = (const uint2 *)P(o.rec); d.rec_rows = (const int *)P(o.rr); d.rec_off = (const long long *)P(o.ro);
-        d.warp_row = (const int *)P(o.wr); d.warp_nsl = (const int *)P(o.wn); d.warp_sl0 = (const int *)P(o.w0);
-        d.sl_off = (const int *)P(o.so); d.sl_len = (const int *)P(o.sl); d.sl_seg = (const int *)P(o.ss);
-        d.segptr = (const int *)P(o.sp); d.nseg = (const int *)P(o.ns);
+        d.warp_row = (const int *)P(o.wr); d.warp_nsl = (const int *)P(o.wn);
     };
     set_sched(gr.fwd, of);
     set_sched(gr.bwd, ob);
@@ -426,7 +422,7 @@ extern "C" fb_status fb_graph_info(fb_graph h, int64_t *out) {
     const Graph &g = h->g;
     int64_t v[16] = {g.G, g.K_tot, g.nnz, g.D, g.T, g.spt, g.mode,
                      (int64_t)smem_bytes(g, false, false), (int64_t)smem_bytes(g, true, true),
-                     g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max, 0, 0};
+                     g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max, g.fwd.rows_max, g.bwd.rows_max};
     std::memcpy(out, v, sizeof v);
     return FB_OK;
 }

@@ -16,33 +16,30 @@ constexpr int kSmemLimit = 227 * 1024;
 
 enum Mode : int { MODE_FACTORED = 0, MODE_EXACT = 1 };
 
-// One direction's arc schedule in sliced-ELL form (forward = in-arcs / CSC of
-// T, backward = out-arcs / CSR; ledger L3).  Rows are cut into segments of at
-// most Lmax arcs; segments sorted by length are grouped 32 at a time into
-// slices (one segment per lane, shorter ones padded with null arcs); slices
-// are packed onto the W warps longest-first.  Every lane of a warp therefore
-// executes the same number of slots with no per-arc control flow.
-//   rec[r*32 + lane] = {byte offset of the other endpoint in the u / p arrays,
-//                       weight: e^{T} (factored) or T·log2(e) (exact)}
-//   member g: records start at rec_off[g]; warp w's slices are
-//   sl_off[g] + warp_sl0[g*W+w] … + warp_nsl[g*W+w], its rows start at
-//   warp_row[g*W+w]; slice q has sl_len[q] rows and lane l reduces into
-//   segment sl_seg[q*32+l] (-1: idle lane).  Segments are numbered in row
-//   order, so state j's segments are [segptr[j], segptr[j+1]).
+// One direction's arc schedule in grouped sliced-ELL form (forward = in-arcs /
+// CSC of T, backward = out-arcs / CSR; ledger L3).  A row (the state being
+// produced) with d arcs is given g = the smallest power of two with
+// ⌈d/g⌉ ≤ Lmax lanes; rows of equal g, sorted by ⌈d/g⌉, form slices of 32/g
+// rows (one lane per row segment).  A slice is one header row of 32 records
+// followed by L data rows (L = the slice's longest segment, rounded up to a
+// multiple of 4 and padded with null arcs); the g partial sums of a row are
+// combined inside the slice by a uniform xor-shuffle, so every state receives
+// exactly one value.  Slices are packed onto warps longest-first; every lane of
+// a warp executes the same instruction stream with no per-arc control flow.
+//   header record:  x = row (state) written by this lane, or 0xFFFFFFFF
+//                   y = g | L << 8                       (warp-uniform)
+//   data record:    x = byte offset of the other endpoint in shared memory
+//                       (p in factored mode, u in exact mode)
+//                   y = weight: e^{T} (factored) or T·log2(e) (exact)
+//   member g: records start at rec_off[g] (rec_rows[g] rows); warp w's
+//   slices start at row warp_row[g*W+w] and there are warp_nsl[g*W+w] of them.
 struct Sched {
     const uint2 *rec = nullptr;
     const int *rec_rows = nullptr;      // [G]
     const long long *rec_off = nullptr; // [G]
     const int *warp_row = nullptr;      // [G*W]
     const int *warp_nsl = nullptr;      // [G*W]
-    const int *warp_sl0 = nullptr;      // [G*W]
-    const int *sl_off = nullptr;        // [G]
-    const int *sl_len = nullptr;        // [Σ slices]
-    const int *sl_seg = nullptr;        // [Σ slices * 32]
-    const int *segptr = nullptr;        // member g at state_off[g] + g, K_g + 1 entries
-    const int *nseg = nullptr;          // [G]
     int rows_max = 0;                   // max rec_rows
-    int nseg_max = 0;
     int slots_max = 0;                  // max rows of one warp
 };
 
@@ -93,15 +90,16 @@ struct SmemLayout {
     size_t rec, u, p, part, gbuf, red, total;
 };
 FBX_HD inline size_t fbx_a16(size_t x) { return (x + 15) & ~size_t(15); }
-FBX_HD inline SmemLayout smem_layout(int rows_max, int K_max, int nseg_max, bool exact, bool gbuf) {
+// Per-state arrays hold K_pad = threads × states-per-thread entries.
+FBX_HD inline SmemLayout smem_layout(int rows_max, int K_pad, bool exact, bool gbuf) {
     const size_t vsz = exact ? 8 : 4;
     SmemLayout L;
     size_t o = 0;
     L.rec = o; o += fbx_a16((size_t)rows_max * 32 * 8);
-    L.u = o; o += fbx_a16((size_t)K_max * vsz);
-    L.p = o; if (!exact) o += fbx_a16((size_t)K_max * 4);
-    L.part = o; o += fbx_a16((size_t)(nseg_max > 0 ? nseg_max : 1) * vsz);
-    L.gbuf = o; if (gbuf) o += fbx_a16((size_t)K_max * 4);
+    L.u = o; o += fbx_a16((size_t)K_pad * vsz);
+    L.p = o; if (!exact) o += fbx_a16((size_t)K_pad * 4);
+    L.part = o; o += fbx_a16((size_t)K_pad * vsz);
+    L.gbuf = o; if (gbuf) o += fbx_a16((size_t)K_pad * 4);
     L.red = o; o += fbx_a16(8 * (2 * 32 + 2 * 64) + 64);
     L.total = o;
     return L;

@@ -144,17 +144,20 @@ __device__ __forceinline__ void warp_lse(V &m, float &s) {
 }
 __device__ __forceinline__ size_t align16d(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Online max-then-sum over one segment column of L records (fallback path of
-// factored mode, where weights are stored as e^{T}).  Accurate libm ops.
-__device__ __noinline__ float exact_segment(const uint2 *col, int L, const unsigned char *smem, unsigned p_minus_u) {
+// Exact max-then-sum over one row held by g lanes (fallback of factored mode,
+// where weights are stored as e^{T}); c0 points at lane `lane0`'s first data
+// record of the slice.  Accurate libm ops; rare.
+__device__ __noinline__ float exact_row(const uint2 *c0, int L, int g, const unsigned char *smem,
+                                        unsigned p_minus_u) {
     float m = NEG_INF, sum = 0.f;
-    for (int s = 0; s < L; ++s) {
-        uint2 r = col[s * 32];
-        float x = *(const float *)(smem + (r.x - p_minus_u)) + log2f(__uint_as_float(r.y));
-        if (x == NEG_INF) continue;
-        if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
-        else sum += exp2f(x - m);
-    }
+    for (int t = 0; t < g; ++t)
+        for (int s = 0; s < L; ++s) {
+            uint2 r = c0[s * 32 + t];
+            float x = *(const float *)(smem + (r.x - p_minus_u)) + log2f(__uint_as_float(r.y));
+            if (x == NEG_INF) continue;
+            if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
+            else sum += exp2f(x - m);
+        }
     return m == NEG_INF ? NEG_INF : m + log2f(sum);
 }
 
@@ -197,7 +200,7 @@ struct Smem {
 template <class V>
 __device__ __forceinline__ Smem<V> carve(unsigned char *base, const Graph &G, bool bwd, bool post, int mode) {
     const Sched &S = bwd ? G.bwd : G.fwd;
-    SmemLayout L = smem_layout(S.rows_max, G.K_max, S.nseg_max, mode == MODE_EXACT, bwd && post);
+    SmemLayout L = smem_layout(S.rows_max, G.T * G.spt, mode == MODE_EXACT, bwd && post);
     Smem<V> m;
     m.rec = (uint2 *)(base + L.rec);
     m.u = (V *)(base + L.u);
@@ -224,76 +227,62 @@ __device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
     return m == ninf<V>() ? ninf<V>() : m + (V)lg2(s);
 }
 
-// Combine the log2 partials of one state's segments.
-template <class V>
-__device__ __forceinline__ V combine_segments(const V *part, int packed) {
-    int seg0 = packed & 0xFFFF, ns = packed >> 16;
-    if (ns == 0) return ninf<V>();
-    V y = part[seg0];
-    if (ns == 1) return y;
-    V m = y;
-    for (int q = 1; q < ns; ++q) m = vmax(m, part[seg0 + q]);
-    if (m == ninf<V>()) return m;
-    float s = 0.f;
-    for (int q = 0; q < ns; ++q) s += ex2((float)(part[seg0 + q] - m));
-    return m + (V)lg2(s);
-}
-
-// Phase A: walk this warp's slices; lane l reduces one row segment per slice.
+// Phase A: walk this warp's slices.  Lane l reduces one row segment per slice;
+// the g lanes of a split row are combined with a uniform xor-shuffle and the
+// group leader writes the row's log2 value into part[row].
 //  factored: Σ p_src · e^{T} (one FMA per arc, two accumulators), exact
 //            fallback when the sum leaves [2^-80, 2^120];
 //  exact:    online max-then-sum in V (double) with one ex2 per arc (two chains).
 template <int MODE, class V>
-__device__ __forceinline__ void phase_a(const uint2 *col, const int *slen, const int *sseg, int nsl,
-                                        const unsigned char *smem, unsigned p_minus_u, V *part) {
+__device__ __forceinline__ void phase_a(const uint2 *col, int nsl, int lane, const unsigned char *smem,
+                                        unsigned p_minus_u, V *part) {
     constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
     constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
-    // records hold byte offsets from the start of dynamic shared memory
-    const unsigned char *ub = smem;
-    const unsigned char *pb = smem;
     for (int q = 0; q < nsl; ++q) {
-        const int L = __ldg(slen + q);
-        const int seg = __ldg(sseg + q * 32);
+        const uint2 h = col[0];
+        const int g = (int)(h.y & 0xFFu), L = (int)(h.y >> 8), row = (int)h.x;
+        const uint2 *c = col + 32;
         if (MODE == MODE_FACTORED) {
             float a0 = 0.f, a1 = 0.f;
-            int s = 0;
-            for (; s + 4 <= L; s += 4) {
-                uint2 r0 = col[(s + 0) * 32], r1 = col[(s + 1) * 32], r2 = col[(s + 2) * 32], r3 = col[(s + 3) * 32];
-                float p0 = *(const float *)(pb + r0.x), p1 = *(const float *)(pb + r1.x);
-                float p2 = *(const float *)(pb + r2.x), p3 = *(const float *)(pb + r3.x);
+            for (int s = 0; s < L; s += 4) {
+                uint2 r0 = c[(s + 0) * 32], r1 = c[(s + 1) * 32], r2 = c[(s + 2) * 32], r3 = c[(s + 3) * 32];
+                float p0 = *(const float *)(smem + r0.x), p1 = *(const float *)(smem + r1.x);
+                float p2 = *(const float *)(smem + r2.x), p3 = *(const float *)(smem + r3.x);
                 a0 = fmaf(p0, __uint_as_float(r0.y), a0);
                 a1 = fmaf(p1, __uint_as_float(r1.y), a1);
                 a0 = fmaf(p2, __uint_as_float(r2.y), a0);
                 a1 = fmaf(p3, __uint_as_float(r3.y), a1);
             }
-            for (; s < L; ++s) {
-                uint2 r = col[s * 32];
-                a0 = fmaf(*(const float *)(pb + r.x), __uint_as_float(r.y), a0);
-            }
             float acc = a0 + a1;
-            if (seg >= 0)
-                part[seg] = (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_segment(col, L, smem, p_minus_u));
+            for (int o = 1; o < g; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (row >= 0)
+                part[row] = (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(c, L, g, smem, p_minus_u));
         } else {
             V m0 = ninf<V>(), m1 = ninf<V>();
             float s0 = 0.f, s1 = 0.f;
-            int s = 0;
             auto push = [&](V &m, float &sm, uint2 r) {
-                V x = *(const V *)(ub + r.x) + (V)__uint_as_float(r.y);
+                V x = *(const V *)(smem + r.x) + (V)__uint_as_float(r.y);
                 V hi = vmax(m, x), lo = vmin(m, x);
                 float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
                 sm = (x > m) ? fmaf(sm, e, 1.f) : sm + e;
                 m = hi;
             };
-            for (; s + 2 <= L; s += 2) {
-                uint2 r0 = col[s * 32], r1 = col[(s + 1) * 32];
+            for (int s = 0; s < L; s += 4) {
+                uint2 r0 = c[(s + 0) * 32], r1 = c[(s + 1) * 32], r2 = c[(s + 2) * 32], r3 = c[(s + 3) * 32];
                 push(m0, s0, r0);
                 push(m1, s1, r1);
+                push(m0, s0, r2);
+                push(m1, s1, r3);
             }
-            if (s < L) push(m0, s0, col[s * 32]);
             lse_combine(m0, s0, m1, s1);
-            if (seg >= 0) part[seg] = (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0);
+            for (int o = 1; o < g; o <<= 1) {
+                V m2 = __shfl_xor_sync(0xffffffffu, m0, o);
+                float s2 = __shfl_xor_sync(0xffffffffu, s0, o);
+                lse_combine(m0, s0, m2, s2);
+            }
+            if (row >= 0) part[row] = (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0);
         }
-        col += L * 32;
+        col = c + L * 32;
     }
 }
 
@@ -405,30 +394,24 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         for (int x = tid; x < n16; x += T) dst[x] = src[x];
     }
     if (tid == 0) sm.flag[0] = 0;
-    const int wsl0 = S.sl_off[gi] + S.warp_sl0[gi * W + warp];
     const int nsl = S.warp_nsl[gi * W + warp];
-    const int *slen = S.sl_len + wsl0;
-    const int *sseg = S.sl_seg + (size_t)wsl0 * 32 + lane;
     const uint2 *mycol = sm.rec + (size_t)S.warp_row[gi * W + warp] * 32 + lane;
     const bool use_mask = BWD ? G.mask_bwd : G.mask_fwd;
     const unsigned p_minus_u = MODE == MODE_FACTORED ? (unsigned)((unsigned char *)sm.p - (unsigned char *)sm.u) : 0u;
 
-    // Owned states j = tid + k*T (k < SPT).  Slots with j ≥ K are inert: no
-    // segments (y = 0̄), pdf 0, never stored.
-    int segp[SPT];      // first segment | count << 16
+    // Owned states j = tid + k*T (k < SPT).  Slots with j ≥ K are inert: their
+    // part entry stays 0̄, pdf 0, never stored to HBM.
     int pdfk[SPT];      // emission column
     int distk[SPT];     // viability distance
-    const int *segptr = S.segptr + s0 + gi;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
         int j = tid + k * T;
-        segp[k] = 0; pdfk[k] = 0; distk[k] = 0;
+        pdfk[k] = 0; distk[k] = 0;
         if (j < K) {
-            int a0 = segptr[j], a1 = segptr[j + 1];
-            segp[k] = a0 | ((a1 - a0) << 16);
             pdfk[k] = G.pdf[s0 + j];
             distk[k] = BWD ? G.dist_start[s0 + j] : G.dist_fin[s0 + j];
         }
+        sm.part[j] = NINF;  // rows without arcs are never written by phase A
     }
     const float *em = a.emis + (size_t)b * a.N_max * a.D;
     const size_t lat_base = (size_t)a.N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
@@ -541,7 +524,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         }
         n = n_next;
         // ---- phase A of frame n
-        phase_a<MODE, V>(mycol, slen, sseg, nsl, smem_raw, p_minus_u, sm.part);
+        phase_a<MODE, V>(mycol, nsl, lane, smem_raw, p_minus_u, sm.part);
         __syncthreads();
         // ---- phase B1 of frame n (+ pending posterior of frame n - dir)
         {
@@ -558,10 +541,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
             V lmax = NINF;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
-                const int ns = segp[k] >> 16;
-                V y = sm.part[segp[k] & 0xFFFF];
-                if (ns > 1) y = combine_segments<V>(sm.part, segp[k]);
-                const bool ok = ns > 0 && viable(k, n);
+                V y = sm.part[tid + k * T];
+                const bool ok = viable(k, n);
                 float v = vcur[k];
                 vsum += v;
                 V v2 = (V)v * L2E;

@@ -101,9 +101,11 @@ def test_c2_numerators(fbx, kind):
 
 # ------------------------------------------------------------------ C3 denominator (G = 1), reduced
 
-@pytest.mark.parametrize("kind,flags", [("uniform", 0), ("softmax4", 0), ("uniform", 1), ("softmax8", 0)])
-def test_c3_den_reduced(fbx, kind, flags):
-    w = synth.make_c3(seed=3, B=6, N=64, kind=kind)
+@pytest.mark.parametrize("kind,flags,K,nnz", [("uniform", 0, 3000, 20000), ("softmax4", 0, 3000, 20000),
+                                              ("softmax8", 0, 3000, 20000), ("uniform", 1, 1500, 10000),
+                                              ("softmax4", 2, 1500, 10000), ("uniform", 0, 700, 4000)])
+def test_c3_den_reduced(fbx, kind, flags, K, nnz):
+    w = synth.make_c3(seed=3, B=6, N=64, kind=kind, K=K, nnz=nnz)
     lens = np.array([64, 1, 33, 64, 17, 50], np.int32)
     r = run_fb(fbx, w.den, w.emis, lens, flags=flags)
     ref = oracle.fb_batch(w.den, w.emis, lens, post=True)
