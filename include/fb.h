@@ -73,7 +73,9 @@ enum {
 enum {
     FB_GRAPH_DEFAULT = 0,
     FB_GRAPH_FORCE_EXACT = 1,    /* every ⊕ row evaluated max-then-sum (one exp per arc) */
-    FB_GRAPH_FORCE_FACTORED = 2  /* exp-factorised ⊕ with exact fallback */
+    FB_GRAPH_FORCE_FACTORED = 2, /* exp-factorised ⊕ with exact fallback */
+    FB_GRAPH_DRY_RUN = 256       /* run the host compiler only: no device allocation; the handle
+                                    supports fb_graph_info/destroy, compute calls reject it */
 };
 
 typedef struct fb_graph_s *fb_graph; /* opaque, immutable after create */

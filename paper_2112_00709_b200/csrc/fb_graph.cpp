@@ -36,11 +36,11 @@ static const int kFar = INT_MAX / 4;
 namespace {
 
 struct HostSched {
-    std::vector<uint2> rec;
-    std::vector<char> is_header;  // per row of 32 records (host only)
-    std::vector<int> rec_rows, warp_row, warp_nsl;
+    std::vector<unsigned char> blob;           // all members, 16-byte aligned each
+    std::vector<std::pair<size_t, size_t>> idx_ranges;  // (byte offset, count) of u16 index words to rebase
+    std::vector<int> rec_bytes, warp_off, warp_nsl;
     std::vector<long long> rec_off;
-    int rows_max = 0, slots_max = 0;
+    int bytes_max = 0, slots_max = 0;
 };
 
 // Arc lists for one member graph in one direction: row r reduces over
@@ -51,8 +51,9 @@ struct RowLists {
 };
 
 // Grouped sliced-ELL schedule for one member graph (appends to hs); see Sched.
-// esize = bytes per element of the gathered u / p arrays; offsets are relative
-// to the gathered array and rebased to shared-memory offsets by the caller.
+// esize = bytes per element of the gathered u / p arrays; index words hold byte
+// offsets relative to the gathered array and are rebased to shared-memory
+// offsets by the caller once the layout is known.
 bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, int Lmax, HostSched &hs) {
     const int W = T / 32;
     struct RowG { int row, len; };
@@ -64,21 +65,22 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
         while (lg < 5 && (d + (1LL << lg) - 1) / (1LL << lg) > Lmax) ++lg;
         cls[lg].push_back({r, (int)((d + (1LL << lg) - 1) / (1LL << lg))});
     }
-    struct Slice { int g, L; std::vector<int> rows; };
+    struct Slice { int lg, L; std::vector<int> rows; };
     std::vector<Slice> sl;
     for (int lg = 0; lg < 6; ++lg) {
         auto &c = cls[lg];
         std::stable_sort(c.begin(), c.end(), [](const RowG &a, const RowG &b) { return a.len > b.len; });
-        const int g = 1 << lg, per = 32 / g;
+        const int per = 32 >> lg;
         for (size_t i = 0; i < c.size(); i += per) {
             Slice s;
-            s.g = g;
-            s.L = (c[i].len + 3) & ~3;
+            s.lg = lg;
+            s.L = (c[i].len + 1) & ~1;
+            if (s.L / 2 >= (1 << 13)) return false;
             for (size_t t = i; t < std::min(c.size(), i + per); ++t) s.rows.push_back(c[t].row);
             sl.push_back(std::move(s));
         }
     }
-    // LPT: longest slice first onto the least-loaded warp
+    // LPT: longest slice first onto the least-loaded warp (cost ≈ slots + slice overhead)
     std::vector<int> order(sl.size());
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sl[a].L > sl[b].L; });
@@ -90,63 +92,71 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
         Item it = heap.top();
         heap.pop();
         wsl[it.second].push_back(q);
-        heap.push({it.first + sl[q].L + 1, it.second});
+        heap.push({it.first + sl[q].L + 4, it.second});
     }
-    std::vector<int> warp_row(W), warp_nsl(W);
-    int rows = 0, slots_max = 0;
+    auto slice_bytes = [](const Slice &s) { return (size_t)128 + (size_t)(s.L / 2) * 384; };
+    std::vector<int> warp_off(W), warp_nsl(W);
+    size_t bytes = 0;
+    int slots_max = 0;
     for (int w = 0; w < W; ++w) {
-        int wr = 0;
-        for (int q : wsl[w]) wr += 1 + sl[q].L;
-        warp_row[w] = rows;
+        warp_off[w] = (int)bytes;
         warp_nsl[w] = (int)wsl[w].size();
-        rows += wr;
-        slots_max = std::max(slots_max, wr);
+        int slots = 0;
+        for (int q : wsl[w]) { bytes += slice_bytes(sl[q]); slots += sl[q].L; }
+        slots_max = std::max(slots_max, slots);
     }
-    const long long off = (long long)hs.rec.size();
-    uint2 pad;
-    pad.x = 0u;
-    float padw = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
-    std::memcpy(&pad.y, &padw, 4);
-    hs.rec.resize(off + (long long)rows * 32, pad);
-    hs.is_header.resize(hs.is_header.size() + rows, 0);
-    const long long hoff = (long long)hs.is_header.size() - rows;
+    if (bytes >= (size_t)1 << 31) return false;
+    const size_t off = hs.blob.size();
+    hs.blob.resize(off + bytes, 0);
+    unsigned char *base = hs.blob.data() + off;
+    const float padw = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
     for (int w = 0; w < W; ++w) {
-        int row = warp_row[w];
+        size_t o = warp_off[w];
         for (int q : wsl[w]) {
             const Slice &s = sl[q];
-            hs.is_header[hoff + row] = 1;
+            const int g = 1 << s.lg, L2 = s.L / 2;
+            int32_t *hdr = (int32_t *)(base + o);
+            uint32_t *idx = (uint32_t *)(base + o + 128);
+            float *wt = (float *)(base + o + 128 + (size_t)L2 * 128);
+            hs.idx_ranges.push_back({off + o + 128, (size_t)L2 * 32});
             for (int l = 0; l < 32; ++l) {
-                int ri = l / s.g, t = l % s.g;
+                int ri = l >> s.lg, t = l & (g - 1);
                 bool has = ri < (int)s.rows.size();
-                uint2 h;
-                h.x = (has && t == 0) ? (uint32_t)s.rows[ri] : 0xFFFFFFFFu;
-                h.y = (uint32_t)s.g | ((uint32_t)s.L << 8);
-                hs.rec[off + (long long)row * 32 + l] = h;
-                if (!has) continue;
-                const int r = s.rows[ri];
-                const long long d = rl.ptr[r + 1] - rl.ptr[r];
-                const long long len = (d + s.g - 1) / s.g;
-                const long long a0 = rl.ptr[r] + t * len, a1 = std::min<long long>(rl.ptr[r + 1], a0 + len);
-                for (long long a = a0; a < a1; ++a) {
-                    uint2 rr;
-                    rr.x = (uint32_t)rl.other[a] * (uint32_t)esize;
-                    double wn = rl.w[a];
-                    float wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
-                    if (std::isinf(wn) && wn < 0) wf = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
-                    std::memcpy(&rr.y, &wf, 4);
-                    hs.rec[off + (long long)(row + 1 + (a - a0)) * 32 + l] = rr;
+                uint32_t lead = (has && t == 0) ? (uint32_t)(s.rows[ri] + 1) : 0u;
+                hdr[l] = (int32_t)(lead | ((uint32_t)s.lg << 16) | ((uint32_t)L2 << 19));
+                long long a0 = 0, a1 = 0;
+                if (has) {
+                    const int r = s.rows[ri];
+                    const long long d = rl.ptr[r + 1] - rl.ptr[r];
+                    const long long len = (d + g - 1) / g;
+                    a0 = std::min<long long>(rl.ptr[r + 1], rl.ptr[r] + t * len);
+                    a1 = std::min<long long>(rl.ptr[r + 1], a0 + len);
+                }
+                for (int sl2 = 0; sl2 < s.L; ++sl2) {
+                    long long a = a0 + sl2;
+                    uint32_t boff = 0;
+                    float wf = padw;
+                    if (a < a1) {
+                        boff = (uint32_t)rl.other[a] * (uint32_t)esize;
+                        double wn = rl.w[a];
+                        wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
+                        if (std::isinf(wn) && wn < 0) wf = padw;
+                    }
+                    uint32_t &word = idx[(sl2 / 2) * 32 + l];
+                    word |= (sl2 & 1) ? (boff << 16) : boff;
+                    wt[((sl2 / 2) * 32 + l) * 2 + (sl2 & 1)] = wf;
                 }
             }
-            row += 1 + s.L;
+            o += slice_bytes(s);
         }
     }
-    hs.rec_off.push_back(off);
-    hs.rec_rows.push_back(rows);
-    hs.warp_row.insert(hs.warp_row.end(), warp_row.begin(), warp_row.end());
+    hs.rec_off.push_back((long long)off);
+    hs.rec_bytes.push_back((int)bytes);
+    hs.warp_off.insert(hs.warp_off.end(), warp_off.begin(), warp_off.end());
     hs.warp_nsl.insert(hs.warp_nsl.end(), warp_nsl.begin(), warp_nsl.end());
-    hs.rows_max = std::max(hs.rows_max, rows);
+    hs.bytes_max = std::max<int>(hs.bytes_max, (int)bytes);
     hs.slots_max = std::max(hs.slots_max, slots_max);
-    return (long long)K * esize < (1LL << 31);
+    return (long long)K * esize <= 65536;  // byte offsets are 16-bit
 }
 
 int pow2ceil(long long x) {
@@ -174,7 +184,7 @@ bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
 
 size_t smem_bytes(const Graph &g, bool backward, bool post) {
     const Sched &s = backward ? g.bwd : g.fwd;
-    return smem_layout(s.rows_max, g.T * g.spt, g.mode == MODE_EXACT, backward && post).total;
+    return smem_layout(s.bytes_max, g.T * g.spt, g.mode == MODE_EXACT, backward && post).total;
 }
 
 }  // namespace fbx
@@ -349,17 +359,11 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         if (dist_fin[i] > 0) gr.mask_fwd = 1;
         if (dist_start[i] > 0) gr.mask_bwd = 1;
     }
-    // records address the gathered array directly: byte offset from the start of
-    // dynamic shared memory (p in factored mode, u in exact mode)
-    for (HostSched *h : {&hf, &hb}) {
-        SmemLayout L = smem_layout(h->rows_max, gr.T * gr.spt, gr.mode == MODE_EXACT, false);
-        const uint32_t base = (uint32_t)(gr.mode == MODE_EXACT ? L.u : L.p);
-        for (size_t row = 0; row < h->is_header.size(); ++row)
-            if (!h->is_header[row])
-                for (int l = 0; l < 32; ++l) h->rec[row * 32 + l].x += base;
-    }
-    gr.fwd.rows_max = hf.rows_max; gr.fwd.slots_max = hf.slots_max;
-    gr.bwd.rows_max = hb.rows_max; gr.bwd.slots_max = hb.slots_max;
+    // index words hold byte offsets relative to the gathered array (p in factored
+    // mode, u in exact mode), which the kernel addresses as [offset + base]
+    gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
+    gr.bwd.bytes_max = hb.bytes_max; gr.bwd.slots_max = hb.slots_max;
+    gr.pm.U_tot = slot_off[G];
     if (smem_bytes(gr, false, false) > (size_t)kSmemLimit || smem_bytes(gr, true, true) > (size_t)kSmemLimit)
         return FB_ERR_UNSUPPORTED;
 
@@ -368,16 +372,33 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     std::vector<int> soff(state_offsets, state_offsets + G + 1);
     size_t o_soff = pk.put(soff), o_pdf = pk.put(pdf), o_i2 = pk.put(init2), o_f2 = pk.put(final2);
     size_t o_df = pk.put(dist_fin), o_ds = pk.put(dist_start);
-    struct SO { size_t rec, rr, ro, wr, wn; };
+    struct SO { size_t rec, rb, ro, wo, wn; };
     auto put_sched = [&](HostSched &h) {
         SO o;
-        o.rec = pk.put(h.rec); o.rr = pk.put(h.rec_rows); o.ro = pk.put(h.rec_off); o.wr = pk.put(h.warp_row);
+        o.rec = pk.put(h.blob); o.rb = pk.put(h.rec_bytes); o.ro = pk.put(h.rec_off); o.wo = pk.put(h.warp_off);
         o.wn = pk.put(h.warp_nsl);
         return o;
     };
     SO of = put_sched(hf), ob = put_sched(hb);
     size_t o_so = pk.put(slot_off), o_spd = pk.put(slot_pdf), o_ssp = pk.put(slot_sptr),
            o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot);
+    if (flags & FB_GRAPH_DRY_RUN) {
+        fb_graph h = new (std::nothrow) fb_graph_s;
+        if (!h) return FB_ERR_NOMEM;
+        gr.dry = true;
+        gr.block_bytes = pk.buf.size();
+        h->g = gr;
+        auto meta = [&](HostSched &hs) {
+            std::vector<int> m;
+            for (int g2 = 0; g2 < G; ++g2) { m.push_back((int)hs.rec_off[g2]); m.push_back(hs.rec_bytes[g2]); }
+            for (size_t w = 0; w < hs.warp_off.size(); ++w) { m.push_back(hs.warp_off[w]); m.push_back(hs.warp_nsl[w]); }
+            return m;
+        };
+        h->host_fwd = hf.blob; h->host_bwd = hb.blob;
+        h->host_fwd_meta = meta(hf); h->host_bwd_meta = meta(hb);
+        *out = h;
+        return FB_OK;
+    }
     void *dev = nullptr;
     cudaGetDevice(&gr.device);
     cudaError_t e = cudaMalloc(&dev, pk.buf.size());
@@ -394,8 +415,8 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.dist_fin = (const int *)P(o_df);
     gr.dist_start = (const int *)P(o_ds);
     auto set_sched = [&](Sched &d, const SO &o) {
-        d.rec = (const uint2 *)P(o.rec); d.rec_rows = (const int *)P(o.rr); d.rec_off = (const long long *)P(o.ro);
-        d.warp_row = (const int *)P(o.wr); d.warp_nsl = (const int *)P(o.wn);
+        d.rec = (const unsigned char *)P(o.rec); d.rec_bytes = (const int *)P(o.rb);
+        d.rec_off = (const long long *)P(o.ro); d.warp_off = (const int *)P(o.wo); d.warp_nsl = (const int *)P(o.wn);
     };
     set_sched(gr.fwd, of);
     set_sched(gr.bwd, ob);
@@ -411,8 +432,10 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
 
 extern "C" fb_status fb_graph_destroy(fb_graph g) {
     if (!g) return FB_OK;
-    cudaDeviceSynchronize();
-    cudaFree(g->g.block);
+    if (!g->g.dry) {
+        cudaDeviceSynchronize();
+        cudaFree(g->g.block);
+    }
     delete g;
     return FB_OK;
 }
@@ -422,7 +445,24 @@ extern "C" fb_status fb_graph_info(fb_graph h, int64_t *out) {
     const Graph &g = h->g;
     int64_t v[16] = {g.G, g.K_tot, g.nnz, g.D, g.T, g.spt, g.mode,
                      (int64_t)smem_bytes(g, false, false), (int64_t)smem_bytes(g, true, true),
-                     g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max, g.fwd.rows_max, g.bwd.rows_max};
+                     g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max, g.fwd.bytes_max, g.bwd.bytes_max};
     std::memcpy(out, v, sizeof v);
     return FB_OK;
+}
+
+// Internal (not part of fb.h): copy a dry-run handle's compiled schedule to the
+// caller for host-side verification.  which = 0 forward, 1 backward.
+// Returns the number of bytes (blob) / ints (meta) available when buffers are NULL.
+extern "C" long long fbx_debug_schedule(fb_graph h, int which, unsigned char *blob, int *meta) {
+    if (!h || !h->g.dry) return -1;
+    const auto &b = which ? h->host_bwd : h->host_fwd;
+    const auto &m = which ? h->host_bwd_meta : h->host_fwd_meta;
+    if (blob) std::memcpy(blob, b.data(), b.size());
+    if (meta) std::memcpy(meta, m.data(), m.size() * sizeof(int));
+    return blob ? (long long)b.size() : (meta ? (long long)m.size() : (long long)b.size() * 0 + (long long)b.size());
+}
+
+extern "C" long long fbx_debug_schedule_meta_len(fb_graph h, int which) {
+    if (!h || !h->g.dry) return -1;
+    return (long long)(which ? h->host_bwd_meta.size() : h->host_fwd_meta.size());
 }

@@ -5,6 +5,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "../../include/fb.h"
 
@@ -18,29 +19,28 @@ enum Mode : int { MODE_FACTORED = 0, MODE_EXACT = 1 };
 
 // One direction's arc schedule in grouped sliced-ELL form (forward = in-arcs /
 // CSC of T, backward = out-arcs / CSR; ledger L3).  A row (the state being
-// produced) with d arcs is given g = the smallest power of two with
-// ⌈d/g⌉ ≤ Lmax lanes; rows of equal g, sorted by ⌈d/g⌉, form slices of 32/g
-// rows (one lane per row segment).  A slice is one header row of 32 records
-// followed by L data rows (L = the slice's longest segment, rounded up to a
-// multiple of 4 and padded with null arcs); the g partial sums of a row are
-// combined inside the slice by a uniform xor-shuffle, so every state receives
-// exactly one value.  Slices are packed onto warps longest-first; every lane of
-// a warp executes the same instruction stream with no per-arc control flow.
-//   header record:  x = row (state) written by this lane, or 0xFFFFFFFF
-//                   y = g | L << 8                       (warp-uniform)
-//   data record:    x = byte offset of the other endpoint in shared memory
-//                       (p in factored mode, u in exact mode)
-//                   y = weight: e^{T} (factored) or T·log2(e) (exact)
-//   member g: records start at rec_off[g] (rec_rows[g] rows); warp w's
-//   slices start at row warp_row[g*W+w] and there are warp_nsl[g*W+w] of them.
+// produced) with d arcs gets g = the smallest power of two with ⌈d/g⌉ ≤ Lmax
+// lanes; rows of equal g, sorted by ⌈d/g⌉, form slices of 32/g rows (one lane
+// per row segment).  The g partial sums of a row are combined inside the slice
+// by a uniform xor-shuffle, so every state receives exactly one value.  Slices
+// are packed onto warps longest-first; every lane of a warp executes the same
+// instruction stream with no per-arc control flow.
+//
+// Byte layout of one slice with L arcs per lane (L even, null-padded):
+//   header  int32[32]        lane l: (row+1 if l leads a row else 0) | log2(g) << 16 | (L/2) << 19
+//   index   uint32[L/2][32]  two u16 byte offsets of the other endpoints in the gathered
+//                            array (p in factored mode, u in exact mode), slot 2i in the low half
+//   weight  float2[L/2][32]  e^{T} (factored) or T·log2(e) (exact) for slots 2i, 2i+1
+// Member g's blob starts at byte rec_off[g] (rec_bytes[g] bytes); warp w's
+// slices start at byte warp_off[g*W+w] of the blob, warp_nsl[g*W+w] of them.
 struct Sched {
-    const uint2 *rec = nullptr;
-    const int *rec_rows = nullptr;      // [G]
+    const unsigned char *rec = nullptr;
+    const int *rec_bytes = nullptr;     // [G]
     const long long *rec_off = nullptr; // [G]
-    const int *warp_row = nullptr;      // [G*W]
+    const int *warp_off = nullptr;      // [G*W]
     const int *warp_nsl = nullptr;      // [G*W]
-    int rows_max = 0;                   // max rec_rows
-    int slots_max = 0;                  // max rows of one warp
+    int bytes_max = 0;                  // max rec_bytes
+    int slots_max = 0;                  // max arc slots of one warp
 };
 
 // Inverse pdf map of each member: slots = distinct pdfs used by the graph, in
@@ -74,6 +74,7 @@ struct Graph {
     PdfMap pm;
     void *block = nullptr;
     size_t block_bytes = 0;
+    bool dry = false;
     int device = 0;
 };
 
@@ -91,15 +92,18 @@ struct SmemLayout {
 };
 FBX_HD inline size_t fbx_a16(size_t x) { return (x + 15) & ~size_t(15); }
 // Per-state arrays hold K_pad = threads × states-per-thread entries.
-FBX_HD inline SmemLayout smem_layout(int rows_max, int K_pad, bool exact, bool gbuf) {
+// In factored mode the γ row of the pdf-level epilogue aliases the partials
+// (each thread reads its own states' partials before writing their γ; k_fb).
+FBX_HD inline SmemLayout smem_layout(int rec_bytes, int K_pad, bool exact, bool gbuf) {
     const size_t vsz = exact ? 8 : 4;
     SmemLayout L;
     size_t o = 0;
-    L.rec = o; o += fbx_a16((size_t)rows_max * 32 * 8);
+    L.rec = o; o += fbx_a16((size_t)rec_bytes);
     L.u = o; o += fbx_a16((size_t)K_pad * vsz);
     L.p = o; if (!exact) o += fbx_a16((size_t)K_pad * 4);
     L.part = o; o += fbx_a16((size_t)K_pad * vsz);
-    L.gbuf = o; if (gbuf) o += fbx_a16((size_t)K_pad * 4);
+    L.gbuf = L.part;
+    if (exact && gbuf) { L.gbuf = o; o += fbx_a16((size_t)K_pad * 4); }
     L.red = o; o += fbx_a16(8 * (2 * 32 + 2 * 64) + 64);
     L.total = o;
     return L;
@@ -112,6 +116,9 @@ size_t smem_bytes(const Graph &g, bool backward, bool pdf_level);
 
 struct fb_graph_s {
     fbx::Graph g;
+    // dry-run handles keep the host image of the compiled schedules for inspection
+    std::vector<unsigned char> host_fwd, host_bwd;
+    std::vector<int> host_fwd_meta, host_bwd_meta;  // per member: rec_off, rec_bytes; then W × (warp_off, warp_nsl)
 };
 
 namespace fbx {

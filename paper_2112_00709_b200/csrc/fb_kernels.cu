@@ -145,15 +145,17 @@ __device__ __forceinline__ void warp_lse(V &m, float &s) {
 __device__ __forceinline__ size_t align16d(size_t x) { return (x + 15) & ~size_t(15); }
 
 // Exact max-then-sum over one row held by g lanes (fallback of factored mode,
-// where weights are stored as e^{T}); c0 points at lane `lane0`'s first data
-// record of the slice.  Accurate libm ops; rare.
-__device__ __noinline__ float exact_row(const uint2 *c0, int L, int g, const unsigned char *smem,
-                                        unsigned p_minus_u) {
+// where weights are stored as e^{T}); idx / wt point at the leader lane's first
+// index word / weight pair of the slice.  Accurate libm ops; rare.
+__device__ __noinline__ float exact_row(const uint32_t *idx, const float2 *wt, int L2, int g, const float *u) {
+    const unsigned char *ub = (const unsigned char *)u;
     float m = NEG_INF, sum = 0.f;
     for (int t = 0; t < g; ++t)
-        for (int s = 0; s < L; ++s) {
-            uint2 r = c0[s * 32 + t];
-            float x = *(const float *)(smem + (r.x - p_minus_u)) + log2f(__uint_as_float(r.y));
+        for (int s = 0; s < 2 * L2; ++s) {
+            uint32_t ix = idx[(s >> 1) * 32 + t];
+            float2 w2 = wt[(s >> 1) * 32 + t];
+            uint32_t off = (s & 1) ? (ix >> 16) : (ix & 0xFFFFu);
+            float x = *(const float *)(ub + off) + log2f((s & 1) ? w2.y : w2.x);
             if (x == NEG_INF) continue;
             if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
             else sum += exp2f(x - m);
@@ -187,7 +189,7 @@ struct FBArgs {
 // Shared-memory carve-up; must match smem_bytes() in fb_graph.cpp.
 template <class V>
 struct Smem {
-    uint2 *rec;
+    unsigned char *rec;
     V *u;
     float *p;
     V *part;
@@ -200,9 +202,9 @@ struct Smem {
 template <class V>
 __device__ __forceinline__ Smem<V> carve(unsigned char *base, const Graph &G, bool bwd, bool post, int mode) {
     const Sched &S = bwd ? G.bwd : G.fwd;
-    SmemLayout L = smem_layout(S.rows_max, G.T * G.spt, mode == MODE_EXACT, bwd && post);
+    SmemLayout L = smem_layout(S.bytes_max, G.T * G.spt, mode == MODE_EXACT, bwd && post);
     Smem<V> m;
-    m.rec = (uint2 *)(base + L.rec);
+    m.rec = base + L.rec;
     m.u = (V *)(base + L.u);
     m.p = mode == MODE_FACTORED ? (float *)(base + L.p) : nullptr;
     m.part = (V *)(base + L.part);
@@ -227,62 +229,65 @@ __device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
     return m == ninf<V>() ? ninf<V>() : m + (V)lg2(s);
 }
 
-// Phase A: walk this warp's slices.  Lane l reduces one row segment per slice;
-// the g lanes of a split row are combined with a uniform xor-shuffle and the
-// group leader writes the row's log2 value into part[row].
+// Phase A: walk this warp's slices (layout in fb_internal.h, Sched).  Lane l
+// reduces one row segment per slice; the g lanes of a split row are combined
+// with a uniform xor-shuffle and the group leader writes the row's log2 value
+// into part[row].
 //  factored: Σ p_src · e^{T} (one FMA per arc, two accumulators), exact
 //            fallback when the sum leaves [2^-80, 2^120];
 //  exact:    online max-then-sum in V (double) with one ex2 per arc (two chains).
 template <int MODE, class V>
-__device__ __forceinline__ void phase_a(const uint2 *col, int nsl, int lane, const unsigned char *smem,
-                                        unsigned p_minus_u, V *part) {
+__device__ __forceinline__ void phase_a(const unsigned char *cur, int nsl, int lane, const V *u, const float *p,
+                                        V *part) {
     constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
     constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
+    const unsigned char *gb = MODE == MODE_FACTORED ? (const unsigned char *)p : (const unsigned char *)u;
     for (int q = 0; q < nsl; ++q) {
-        const uint2 h = col[0];
-        const int g = (int)(h.y & 0xFFu), L = (int)(h.y >> 8), row = (int)h.x;
-        const uint2 *c = col + 32;
+        const int h = ((const int *)cur)[lane];
+        const int row = (h & 0xFFFF) - 1, lg = (h >> 16) & 7, L2 = (int)((unsigned)h >> 19);
+        const uint32_t *idx = (const uint32_t *)(cur + 128) + lane;
+        const float2 *wt = (const float2 *)(cur + 128 + (size_t)L2 * 128) + lane;
         if (MODE == MODE_FACTORED) {
             float a0 = 0.f, a1 = 0.f;
-            for (int s = 0; s < L; s += 4) {
-                uint2 r0 = c[(s + 0) * 32], r1 = c[(s + 1) * 32], r2 = c[(s + 2) * 32], r3 = c[(s + 3) * 32];
-                float p0 = *(const float *)(smem + r0.x), p1 = *(const float *)(smem + r1.x);
-                float p2 = *(const float *)(smem + r2.x), p3 = *(const float *)(smem + r3.x);
-                a0 = fmaf(p0, __uint_as_float(r0.y), a0);
-                a1 = fmaf(p1, __uint_as_float(r1.y), a1);
-                a0 = fmaf(p2, __uint_as_float(r2.y), a0);
-                a1 = fmaf(p3, __uint_as_float(r3.y), a1);
+#pragma unroll 2
+            for (int s = 0; s < L2; ++s) {
+                const uint32_t ix = idx[s * 32];
+                const float2 w2 = wt[s * 32];
+                const float p0 = *(const float *)(gb + (ix & 0xFFFFu));
+                const float p1 = *(const float *)(gb + (ix >> 16));
+                a0 = fmaf(p0, w2.x, a0);
+                a1 = fmaf(p1, w2.y, a1);
             }
             float acc = a0 + a1;
-            for (int o = 1; o < g; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            for (int o = 1; o < (1 << lg); o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (row >= 0)
-                part[row] = (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(c, L, g, smem, p_minus_u));
+                part[row] = (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc)
+                                                               : exact_row(idx, wt, L2, 1 << lg, (const float *)u));
         } else {
             V m0 = ninf<V>(), m1 = ninf<V>();
             float s0 = 0.f, s1 = 0.f;
-            auto push = [&](V &m, float &sm, uint2 r) {
-                V x = *(const V *)(smem + r.x) + (V)__uint_as_float(r.y);
+            auto push = [&](V &m, float &sm, uint32_t off, float w) {
+                V x = *(const V *)(gb + off) + (V)w;
                 V hi = vmax(m, x), lo = vmin(m, x);
                 float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
                 sm = (x > m) ? fmaf(sm, e, 1.f) : sm + e;
                 m = hi;
             };
-            for (int s = 0; s < L; s += 4) {
-                uint2 r0 = c[(s + 0) * 32], r1 = c[(s + 1) * 32], r2 = c[(s + 2) * 32], r3 = c[(s + 3) * 32];
-                push(m0, s0, r0);
-                push(m1, s1, r1);
-                push(m0, s0, r2);
-                push(m1, s1, r3);
+            for (int s = 0; s < L2; ++s) {
+                const uint32_t ix = idx[s * 32];
+                const float2 w2 = wt[s * 32];
+                push(m0, s0, ix & 0xFFFFu, w2.x);
+                push(m1, s1, ix >> 16, w2.y);
             }
             lse_combine(m0, s0, m1, s1);
-            for (int o = 1; o < g; o <<= 1) {
+            for (int o = 1; o < (1 << lg); o <<= 1) {
                 V m2 = __shfl_xor_sync(0xffffffffu, m0, o);
                 float s2 = __shfl_xor_sync(0xffffffffu, s0, o);
                 lse_combine(m0, s0, m2, s2);
             }
             if (row >= 0) part[row] = (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0);
         }
-        col = c + L * 32;
+        cur += 128 + (size_t)L2 * 384;
     }
 }
 
@@ -390,14 +395,13 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     {
         const uint4 *src = (const uint4 *)(S.rec + S.rec_off[gi]);
         uint4 *dst = (uint4 *)sm.rec;
-        const int n16 = S.rec_rows[gi] * 16;
+        const int n16 = S.rec_bytes[gi] >> 4;
         for (int x = tid; x < n16; x += T) dst[x] = src[x];
     }
     if (tid == 0) sm.flag[0] = 0;
     const int nsl = S.warp_nsl[gi * W + warp];
-    const uint2 *mycol = sm.rec + (size_t)S.warp_row[gi * W + warp] * 32 + lane;
+    const unsigned char *mysl = sm.rec + S.warp_off[gi * W + warp];
     const bool use_mask = BWD ? G.mask_bwd : G.mask_fwd;
-    const unsigned p_minus_u = MODE == MODE_FACTORED ? (unsigned)((unsigned char *)sm.p - (unsigned char *)sm.u) : 0u;
 
     // Owned states j = tid + k*T (k < SPT).  Slots with j ≥ K are inert: their
     // part entry stays 0̄, pdf 0, never stored to HBM.
@@ -524,20 +528,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         }
         n = n_next;
         // ---- phase A of frame n
-        phase_a<MODE, V>(mycol, nsl, lane, smem_raw, p_minus_u, sm.part);
+        phase_a<MODE, V>(mysl, nsl, lane, sm.u, sm.p, sm.part);
         __syncthreads();
         // ---- phase B1 of frame n (+ pending posterior of frame n - dir)
         {
-            if (pend) {
-                V Z = block_lse_from<V>(sm.wz + (step & 1) * 64, W, lane);
-                float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pend_n * K : sm.gbuf;
-#pragma unroll
-                for (int k = 0; k < SPT; ++k) {
-                    int j = tid + k * T;
-                    float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
-                    if (j < K) prow[j] = gam;
-                }
-            }
             V lmax = NINF;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
@@ -557,6 +551,17 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
             }
             lmax = warp_max(lmax);
             if (lane == 0) sm.wmax[((step + 1) & 1) * 32 + warp] = (double)lmax;
+            // γ of the pending frame; gbuf may alias part, so only after the reads above
+            if (pend) {
+                V Z = block_lse_from<V>(sm.wz + (step & 1) * 64, W, lane);
+                float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pend_n * K : sm.gbuf;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) {
+                    int j = tid + k * T;
+                    float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
+                    if (j < K) prow[j] = gam;
+                }
+            }
         }
         __syncthreads();
         if (pdf_post && pend) pdf_row(a, sm.gbuf, gi, b, pend_n, tid, T);
@@ -803,7 +808,7 @@ extern "C" fb_status fb_forward(fb_graph g, const float *log_emis, const int32_t
                                 int32_t N_max, float *alpha, double *alpha_scale, double *logZ,
                                 int32_t *seq_status, void *stream) {
     if (!g || !log_emis || !lengths || !logZ || !seq_status || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
-    if (!(g->g.G == 1 || g->g.G == B)) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B) || g->g.dry) return FB_ERR_INVALID_ARG;
     if (alpha && !alpha_scale) return FB_ERR_INVALID_ARG;
     FBArgs a = base_args(g, log_emis, lengths, B, N_max);
     a.lat = alpha;
@@ -818,7 +823,7 @@ extern "C" fb_status fb_backward(fb_graph g, const float *log_emis, const int32_
                                  const float *alpha, float *post, int32_t pdf_level, int32_t *seq_status,
                                  void *stream) {
     if (!g || !log_emis || !lengths || !seq_status || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
-    if (!(g->g.G == 1 || g->g.G == B)) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B) || g->g.dry) return FB_ERR_INVALID_ARG;
     if (post && !alpha) return FB_ERR_INVALID_ARG;
     if (pdf_level != 0 && pdf_level != 1) return FB_ERR_INVALID_ARG;
     FBArgs a = base_args(g, log_emis, lengths, B, N_max);
@@ -836,7 +841,7 @@ extern "C" fb_status fb_posteriors(fb_graph g, const float *alpha, const float *
                                    const int32_t *seq_status, int32_t B, int32_t N_max, int32_t pdf_level,
                                    float *post, void *stream) {
     if (!g || !alpha || !beta || !lengths || !post || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
-    if (!(g->g.G == 1 || g->g.G == B)) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B) || g->g.dry) return FB_ERR_INVALID_ARG;
     if (pdf_level != 0 && pdf_level != 1) return FB_ERR_INVALID_ARG;
     const Graph &G = g->g;
     cudaStream_t s = (cudaStream_t)stream;
@@ -862,7 +867,8 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
                                      void *stream) {
     if (!num || !den || !log_emis || !lengths || !grad || !loss || !totals || !seq_status || B < 1 || N_max < 1)
         return FB_ERR_INVALID_ARG;
-    if (num->g.G != B || den->g.G != 1 || num->g.D != den->g.D) return FB_ERR_INVALID_ARG;
+    if (num->g.G != B || den->g.G != 1 || num->g.D != den->g.D || num->g.dry || den->g.dry)
+        return FB_ERR_INVALID_ARG;
     WsLayout L = ws_layout(num->g, den->g, B, N_max);
     if (!workspace || workspace_bytes < L.total) return FB_ERR_WORKSPACE;
     unsigned char *ws = (unsigned char *)workspace;

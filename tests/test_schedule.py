@@ -1,0 +1,162 @@
+"""Host graph compiler (fb_graph_create, FB_GRAPH_DRY_RUN) checked on CPU.
+
+The compiled grouped sliced-ELL schedules (fb_internal.h, Sched) are decoded
+here exactly the way phase A of k_fb walks them, and every state's reduction
+must see precisely its arcs: in-arcs (CSC of T) for the forward, out-arcs
+(CSR) for the backward (ledger L3), with the stored weight e^{T} (factored) or
+T·log2(e) (exact).  Also checks that every BASELINE workload graph compiles
+within the shared-memory budget.
+"""
+import ctypes
+from collections import Counter
+
+import numpy as np
+import pytest
+
+from paper_2112_00709_b200 import synth
+
+DRY = 256
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2112_00709_b200 import build
+
+    build.build()
+    from paper_2112_00709_b200 import _lib
+
+    lib = _lib.lib()
+    lib.fbx_debug_schedule.restype = ctypes.c_longlong
+    lib.fbx_debug_schedule.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    lib.fbx_debug_schedule_meta_len.restype = ctypes.c_longlong
+    lib.fbx_debug_schedule_meta_len.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    return lib
+
+
+def compile_dry(L, g, flags=0):
+    from paper_2112_00709_b200 import _np_ptr
+
+    so = np.ascontiguousarray(g.state_offsets if hasattr(g, "state_offsets") else [0, g.K], np.int32)
+    arrs = [np.ascontiguousarray(x, t) for x, t in [(so, np.int32), (g.row_ptr, np.int32), (g.col, np.int32),
+                                                     (g.logw, np.float32), (g.log_init, np.float32),
+                                                     (g.log_final, np.float32), (g.pdf_of, np.int32)]]
+    h = ctypes.c_void_p()
+    code = L.fb_graph_create(ctypes.byref(h), len(so) - 1, *[_np_ptr(a) for a in arrs], g.D, flags | DRY)
+    info = np.zeros(16, np.int64)
+    if code == 0:
+        L.fb_graph_info(h, _np_ptr(info))
+    return code, h, info
+
+
+def decode(L, h, which, G, W, exact):
+    n = L.fbx_debug_schedule(h, which, None, None)
+    blob = np.zeros(n, np.uint8)
+    m = L.fbx_debug_schedule_meta_len(h, which)
+    meta = np.zeros(m, np.int32)
+    L.fbx_debug_schedule(h, which, blob.ctypes.data_as(ctypes.c_void_p), None)
+    L.fbx_debug_schedule(h, which, None, meta.ctypes.data_as(ctypes.c_void_p))
+    esize = 8 if exact else 4
+    pad = -np.inf if exact else 0.0
+    rows = [dict() for _ in range(G)]
+    for g in range(G):
+        off, nbytes = meta[2 * g], meta[2 * g + 1]
+        for w in range(W):
+            woff, nsl = meta[2 * G + 2 * (g * W + w)], meta[2 * G + 2 * (g * W + w) + 1]
+            cur = off + woff
+            for _ in range(nsl):
+                hdr = blob[cur:cur + 128].view(np.int32)
+                lg = (hdr[0] >> 16) & 7
+                L2 = int(np.uint32(hdr[0]) >> 19)
+                assert ((hdr >> 16) & 7 == lg).all() and (np.uint32(hdr) >> 19 == L2).all()  # uniform
+                idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint32).reshape(L2, 32)
+                wt = blob[cur + 128 + L2 * 128:cur + 128 + L2 * 384].view(np.float32).reshape(L2, 32, 2)
+                gsz = 1 << lg
+                for lane in range(32):
+                    lead = (hdr[lane] & 0xFFFF) - 1
+                    if lead < 0:
+                        continue
+                    assert lane % gsz == 0
+                    arcs = []
+                    for t in range(lane, lane + gsz):
+                        for s in range(2 * L2):
+                            word = int(idx[s // 2, t])
+                            o = (word >> 16) if (s & 1) else (word & 0xFFFF)
+                            wv = float(wt[s // 2, t, s & 1])
+                            if wv == pad:
+                                continue
+                            assert o % esize == 0
+                            arcs.append((o // esize, wv))
+                    assert lead not in rows[g], "row written twice"
+                    rows[g][lead] = Counter(arcs)
+                cur += 128 + L2 * 384
+            assert cur <= off + nbytes
+    return rows
+
+
+def expected(g_member, which, exact):
+    src, dst, w = g_member.arcs()
+    out = {}
+    for i, j, t in zip(src.tolist(), dst.tolist(), w.tolist()):
+        if t == -np.inf:
+            continue
+        enc = float(np.float32(np.float64(t) * 1.4426950408889634)) if exact else float(np.float32(np.exp(np.float64(t))))
+        if enc == (0.0 if not exact else -np.inf):
+            continue
+        row, other = (j, i) if which == 0 else (i, j)
+        out.setdefault(row, Counter())[(other, enc)] += 1
+    return out
+
+
+def check_graph(L, comp, flags=0):
+    code, h, info = compile_dry(L, comp, flags)
+    assert code == 0, code
+    G, T, mode = int(info[0]), int(info[4]), int(info[6])
+    exact = mode == 1
+    members = comp.members if hasattr(comp, "members") and comp.members else [comp]
+    for which in (0, 1):
+        rows = decode(L, h, which, G, T // 32, exact)
+        for gi, m in enumerate(members):
+            exp = expected(m, which, exact)
+            got = {r: c for r, c in rows[gi].items() if sum(c.values())}
+            assert got == exp, (gi, which)
+    assert info[7] <= 227 * 1024 and info[8] <= 227 * 1024
+    L.fb_graph_destroy(h)
+    return info
+
+
+def test_c1_and_random_small(L):
+    for seed in range(10):
+        check_graph(L, synth.make_c1(seed).den)
+        rng = np.random.default_rng(seed)
+        g = synth.random_small_graph(rng, K=int(rng.integers(1, 7)), D=4)
+        check_graph(L, g, flags=1)
+
+
+def test_c2_numerators(L):
+    w = synth.make_c2(seed=2)
+    info = check_graph(L, synth.compose(w.nums))
+    assert info[6] == 1  # exact mode for left-to-right numerators
+
+
+@pytest.mark.parametrize("flags", [0, 2])
+def test_c3_den(L, flags):
+    den = synth.make_den(3)
+    info = check_graph(L, den, flags)
+    assert info[6] == 0 and info[4] == 1024
+
+
+def test_c4_den_and_nums(L):
+    w = synth.make_c4(seed=4, B=16, N=10)
+    check_graph(L, w.den)
+    check_graph(L, synth.compose(w.nums))
+
+
+def test_hub_rows_split_across_lanes(L):
+    # one state with 200 in-arcs forces g > 1 groups
+    K = 300
+    src = list(range(K)) + list(range(1, K)) + [i for i in range(K) if i % 3 == 0]
+    dst = list(range(K)) + [0] * (K - 1) + [5] * len([i for i in range(K) if i % 3 == 0])
+    rng = np.random.default_rng(0)
+    g = synth.graph_from_arcs(K, src, dst, rng.uniform(-3, 0, len(src)), np.zeros(K), np.zeros(K))
+    check_graph(L, g, flags=2)
+    check_graph(L, g, flags=1)
