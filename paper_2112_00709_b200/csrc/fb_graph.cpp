@@ -37,7 +37,6 @@ namespace {
 
 struct HostSched {
     std::vector<unsigned char> blob;           // all members, 16-byte aligned each
-    std::vector<std::pair<size_t, size_t>> idx_ranges;  // (byte offset, count) of u16 index words to rebase
     std::vector<int> rec_bytes, warp_off, warp_nsl;
     std::vector<long long> rec_off;
     int bytes_max = 0, slots_max = 0;
@@ -116,9 +115,8 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
             const Slice &s = sl[q];
             const int g = 1 << s.lg, L2 = s.L / 2;
             int32_t *hdr = (int32_t *)(base + o);
-            uint32_t *idx = (uint32_t *)(base + o + 128);
+            uint16_t *idx = (uint16_t *)(base + o + 128);
             float *wt = (float *)(base + o + 128 + (size_t)L2 * 128);
-            hs.idx_ranges.push_back({off + o + 128, (size_t)L2 * 32});
             for (int l = 0; l < 32; ++l) {
                 int ri = l >> s.lg, t = l & (g - 1);
                 bool has = ri < (int)s.rows.size();
@@ -142,8 +140,7 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
                         wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
                         if (std::isinf(wn) && wn < 0) wf = padw;
                     }
-                    uint32_t &word = idx[(sl2 / 2) * 32 + l];
-                    word |= (sl2 & 1) ? (boff << 16) : boff;
+                    idx[sl2 * 32 + l] = (uint16_t)boff;
                     wt[((sl2 / 2) * 32 + l) * 2 + (sl2 & 1)] = wf;
                 }
             }

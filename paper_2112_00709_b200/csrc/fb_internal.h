@@ -28,8 +28,8 @@ enum Mode : int { MODE_FACTORED = 0, MODE_EXACT = 1 };
 //
 // Byte layout of one slice with L arcs per lane (L even, null-padded):
 //   header  int32[32]        lane l: (row+1 if l leads a row else 0) | log2(g) << 16 | (L/2) << 19
-//   index   uint32[L/2][32]  two u16 byte offsets of the other endpoints in the gathered
-//                            array (p in factored mode, u in exact mode), slot 2i in the low half
+//   index   uint16[L][32]    byte offset of the other endpoint in the gathered array
+//                            (p in factored mode, u in exact mode)
 //   weight  float2[L/2][32]  e^{T} (factored) or T·log2(e) (exact) for slots 2i, 2i+1
 // Member g's blob starts at byte rec_off[g] (rec_bytes[g] bytes); warp w's
 // slices start at byte warp_off[g*W+w] of the blob, warp_nsl[g*W+w] of them.
@@ -92,8 +92,6 @@ struct SmemLayout {
 };
 FBX_HD inline size_t fbx_a16(size_t x) { return (x + 15) & ~size_t(15); }
 // Per-state arrays hold K_pad = threads × states-per-thread entries.
-// In factored mode the γ row of the pdf-level epilogue aliases the partials
-// (each thread reads its own states' partials before writing their γ; k_fb).
 FBX_HD inline SmemLayout smem_layout(int rec_bytes, int K_pad, bool exact, bool gbuf) {
     const size_t vsz = exact ? 8 : 4;
     SmemLayout L;
@@ -102,8 +100,7 @@ FBX_HD inline SmemLayout smem_layout(int rec_bytes, int K_pad, bool exact, bool 
     L.u = o; o += fbx_a16((size_t)K_pad * vsz);
     L.p = o; if (!exact) o += fbx_a16((size_t)K_pad * 4);
     L.part = o; o += fbx_a16((size_t)K_pad * vsz);
-    L.gbuf = L.part;
-    if (exact && gbuf) { L.gbuf = o; o += fbx_a16((size_t)K_pad * 4); }
+    L.gbuf = o; if (gbuf) o += fbx_a16((size_t)K_pad * 4);
     L.red = o; o += fbx_a16(8 * (2 * 32 + 2 * 64) + 64);
     L.total = o;
     return L;

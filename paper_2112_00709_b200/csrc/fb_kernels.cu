@@ -142,25 +142,46 @@ __device__ __forceinline__ void warp_lse(V &m, float &s) {
         lse_combine(m, s, m2, s2);
     }
 }
-__device__ __forceinline__ size_t align16d(size_t x) { return (x + 15) & ~size_t(15); }
 
-// Exact max-then-sum over one row held by g lanes (fallback of factored mode,
-// where weights are stored as e^{T}); idx / wt point at the leader lane's first
-// index word / weight pair of the slice.  Accurate libm ops; rare.
-__device__ __noinline__ float exact_row(const uint32_t *idx, const float2 *wt, int L2, int g, const float *u) {
-    const unsigned char *ub = (const unsigned char *)u;
-    float m = NEG_INF, sum = 0.f;
-    for (int t = 0; t < g; ++t)
-        for (int s = 0; s < 2 * L2; ++s) {
-            uint32_t ix = idx[(s >> 1) * 32 + t];
-            float2 w2 = wt[(s >> 1) * 32 + t];
-            uint32_t off = (s & 1) ? (ix >> 16) : (ix & 0xFFFFu);
-            float x = *(const float *)(ub + off) + log2f((s & 1) ? w2.y : w2.x);
-            if (x == NEG_INF) continue;
-            if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
-            else sum += exp2f(x - m);
-        }
-    return m == NEG_INF ? NEG_INF : m + log2f(sum);
+// Shared-memory access through 32-bit shared-window addresses (explicit PTX so
+// the hot loops carry no generic-address arithmetic).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return (uint32_t)v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_v(uint32_t a, float) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_v(uint32_t a, double) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_v(uint32_t a, float v) { asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v)); }
+__device__ __forceinline__ void sts_v(uint32_t a, double v) { asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v)); }
+__device__ __forceinline__ void sts_i(uint32_t a, int v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ int lds_i(uint32_t a) { return (int)lds_u32(a); }
+
+// Block log-sum-exp from per-warp (m, s) pairs in (generic) shared memory.
+template <class V>
+__device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
+    V m = lane < W ? (V)wz[2 * lane] : ninf<V>();
+    float s = lane < W ? (float)wz[2 * lane + 1] : 0.f;
+    warp_lse(m, s);
+    return m == ninf<V>() ? ninf<V>() : m + (V)lg2(s);
 }
 
 // Output kinds of the backward posterior epilogue.
@@ -186,50 +207,24 @@ struct FBArgs {
     const int *num_pdf_slot; // [B*D]
 };
 
-// Shared-memory carve-up; must match smem_bytes() in fb_graph.cpp.
-template <class V>
-struct Smem {
-    unsigned char *rec;
-    V *u;
-    float *p;
-    V *part;
-    float *gbuf;
-    double *wmax;  // [2][32]
-    double *wz;    // [2][32][2]  (m, s) per warp
-    int *flag;
-};
-
-template <class V>
-__device__ __forceinline__ Smem<V> carve(unsigned char *base, const Graph &G, bool bwd, bool post, int mode) {
-    const Sched &S = bwd ? G.bwd : G.fwd;
-    SmemLayout L = smem_layout(S.bytes_max, G.T * G.spt, mode == MODE_EXACT, bwd && post);
-    Smem<V> m;
-    m.rec = base + L.rec;
-    m.u = (V *)(base + L.u);
-    m.p = mode == MODE_FACTORED ? (float *)(base + L.p) : nullptr;
-    m.part = (V *)(base + L.part);
-    m.gbuf = (bwd && post) ? (float *)(base + L.gbuf) : nullptr;
-    m.wmax = (double *)(base + L.red);
-    m.wz = m.wmax + 64;
-    m.flag = (int *)(m.wz + 128);
-    return m;
+// Exact max-then-sum over one row held by g lanes (fallback of factored mode,
+// where weights are stored as e^{T}); `cur` is the slice, `lane` the group
+// leader.  Accurate libm ops; rare.
+__device__ __noinline__ float exact_row(uint32_t cur, int L2, int g, int lane, uint32_t a_u) {
+    float m = NEG_INF, sum = 0.f;
+    for (int t = 0; t < g; ++t)
+        for (int s = 0; s < 2 * L2; ++s) {
+            uint32_t o = lds_u16(cur + 128 + s * 64 + (lane + t) * 2);
+            float w = lds_v(cur + 128 + L2 * 128 + (s >> 1) * 256 + (lane + t) * 8 + (s & 1) * 4, 0.f);
+            float x = lds_v(a_u + o, 0.f) + log2f(w);
+            if (x == NEG_INF) continue;
+            if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
+            else sum += exp2f(x - m);
+        }
+    return m == NEG_INF ? NEG_INF : m + log2f(sum);
 }
 
-// Block-wide reductions over per-warp partials w[0..W-1] (every warp computes them).
-template <class V>
-__device__ __forceinline__ V block_max_from(const double *w, int W, int lane) {
-    V v = lane < W ? (V)w[lane] : ninf<V>();
-    return warp_max(v);
-}
-template <class V>
-__device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
-    V m = lane < W ? (V)wz[2 * lane] : ninf<V>();
-    float s = lane < W ? (float)wz[2 * lane + 1] : 0.f;
-    warp_lse(m, s);
-    return m == ninf<V>() ? ninf<V>() : m + (V)lg2(s);
-}
-
-// Phase A: walk this warp's slices (layout in fb_internal.h, Sched).  Lane l
+// Phase A: walk this warp's slices (layout: fb_internal.h, Sched).  Lane l
 // reduces one row segment per slice; the g lanes of a split row are combined
 // with a uniform xor-shuffle and the group leader writes the row's log2 value
 // into part[row].
@@ -237,47 +232,52 @@ __device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
 //            fallback when the sum leaves [2^-80, 2^120];
 //  exact:    online max-then-sum in V (double) with one ex2 per arc (two chains).
 template <int MODE, class V>
-__device__ __forceinline__ void phase_a(const unsigned char *cur, int nsl, int lane, const V *u, const float *p,
-                                        V *part) {
+__device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_t a_u, uint32_t a_p,
+                                        uint32_t a_part) {
     constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
     constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
-    const unsigned char *gb = MODE == MODE_FACTORED ? (const unsigned char *)p : (const unsigned char *)u;
+    constexpr uint32_t VS = sizeof(V);
     for (int q = 0; q < nsl; ++q) {
-        const int h = ((const int *)cur)[lane];
-        const int row = (h & 0xFFFF) - 1, lg = (h >> 16) & 7, L2 = (int)((unsigned)h >> 19);
-        const uint32_t *idx = (const uint32_t *)(cur + 128) + lane;
-        const float2 *wt = (const float2 *)(cur + 128 + (size_t)L2 * 128) + lane;
+        const uint32_t h = lds_u32(cur + lane * 4);
+        const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
+        uint32_t ia = cur + 128 + lane * 2;
+        uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
         if (MODE == MODE_FACTORED) {
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll 2
             for (int s = 0; s < L2; ++s) {
-                const uint32_t ix = idx[s * 32];
-                const float2 w2 = wt[s * 32];
-                const float p0 = *(const float *)(gb + (ix & 0xFFFFu));
-                const float p1 = *(const float *)(gb + (ix >> 16));
+                const uint32_t o0 = lds_u16(ia), o1 = lds_u16(ia + 64);
+                const float2 w2 = lds_f2(wa);
+                const float p0 = lds_v(a_p + o0, 0.f), p1 = lds_v(a_p + o1, 0.f);
                 a0 = fmaf(p0, w2.x, a0);
                 a1 = fmaf(p1, w2.y, a1);
+                ia += 128;
+                wa += 256;
             }
             float acc = a0 + a1;
-            for (int o = 1; o < (1 << lg); o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lg) {
+                for (int o = 1; o < (1 << lg); o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            }
             if (row >= 0)
-                part[row] = (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc)
-                                                               : exact_row(idx, wt, L2, 1 << lg, (const float *)u));
+                sts_v(a_part + (uint32_t)row * VS,
+                      (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(cur, L2, 1 << lg, lane, a_u)));
         } else {
             V m0 = ninf<V>(), m1 = ninf<V>();
             float s0 = 0.f, s1 = 0.f;
             auto push = [&](V &m, float &sm, uint32_t off, float w) {
-                V x = *(const V *)(gb + off) + (V)w;
+                V x = lds_v(a_u + off, (V)0) + (V)w;
                 V hi = vmax(m, x), lo = vmin(m, x);
                 float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
                 sm = (x > m) ? fmaf(sm, e, 1.f) : sm + e;
                 m = hi;
             };
             for (int s = 0; s < L2; ++s) {
-                const uint32_t ix = idx[s * 32];
-                const float2 w2 = wt[s * 32];
-                push(m0, s0, ix & 0xFFFFu, w2.x);
-                push(m1, s1, ix >> 16, w2.y);
+                const uint32_t o0 = lds_u16(ia), o1 = lds_u16(ia + 64);
+                const float2 w2 = lds_f2(wa);
+                push(m0, s0, o0, w2.x);
+                push(m1, s1, o1, w2.y);
+                ia += 128;
+                wa += 256;
             }
             lse_combine(m0, s0, m1, s1);
             for (int o = 1; o < (1 << lg); o <<= 1) {
@@ -285,9 +285,9 @@ __device__ __forceinline__ void phase_a(const unsigned char *cur, int nsl, int l
                 float s2 = __shfl_xor_sync(0xffffffffu, s0, o);
                 lse_combine(m0, s0, m2, s2);
             }
-            if (row >= 0) part[row] = (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0);
+            if (row >= 0) sts_v(a_part + (uint32_t)row * VS, (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0));
         }
-        cur += 128 + (size_t)L2 * 384;
+        cur += 128 + (uint32_t)L2 * 384;
     }
 }
 
@@ -355,9 +355,17 @@ __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, in
 
 // ------------------------------------------------------------------ forward / backward kernel
 
+// One CTA runs the whole recursion of one sequence in one direction.  Per frame:
+//   phase A (arcs) → barrier → phase B (states) → barrier.
+// Phase B normalises with the lagged constant c_n = max of the previous
+// frame's vector (known after the barrier, no extra reduction pass); the
+// float64 offset accumulates c_n exactly, and the largest entry of each stored
+// frame is the one-frame change of the recursion, so exp2 of the vector stays
+// in range (exact fallback otherwise).
 template <bool BWD, int MODE, int SPT, int MAXT>
 __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArgs a) {
     using V = typename std::conditional<MODE == MODE_EXACT, double, float>::type;
+    constexpr uint32_t VS = sizeof(V);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Graph &G = a.g;
     const int b = blockIdx.x;
@@ -369,7 +377,11 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     const Sched &S = BWD ? G.bwd : G.fwd;
     const bool want_post = BWD && a.post_kind != POST_NONE;
     const bool pdf_post = want_post && a.post_kind != POST_STATE;
-    Smem<V> sm = carve<V>(smem_raw, G, BWD, want_post, MODE);
+    const SmemLayout SL = smem_layout(S.bytes_max, T * SPT, MODE == MODE_EXACT, want_post && pdf_post);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t a_u = sb + (uint32_t)SL.u, a_p = sb + (uint32_t)SL.p, a_part = sb + (uint32_t)SL.part;
+    const uint32_t a_wmax = sb + (uint32_t)SL.red, a_wz = a_wmax + 64 * 8, a_flag = a_wmax + 192 * 8;
+    float *gbuf = (float *)(smem_raw + SL.gbuf);
     const V L2E = (V)1.4426950408889634;
     const V LN2 = (V)0.6931471805599453;
     const V NINF = ninf<V>();
@@ -394,28 +406,29 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     // schedule → shared memory (16-byte vector copy)
     {
         const uint4 *src = (const uint4 *)(S.rec + S.rec_off[gi]);
-        uint4 *dst = (uint4 *)sm.rec;
+        uint4 *dst = (uint4 *)(smem_raw + SL.rec);
         const int n16 = S.rec_bytes[gi] >> 4;
         for (int x = tid; x < n16; x += T) dst[x] = src[x];
     }
-    if (tid == 0) sm.flag[0] = 0;
+    if (tid == 0) sts_i(a_flag, 0);
     const int nsl = S.warp_nsl[gi * W + warp];
-    const unsigned char *mysl = sm.rec + S.warp_off[gi * W + warp];
+    const uint32_t mysl = sb + (uint32_t)SL.rec + (uint32_t)S.warp_off[gi * W + warp];
     const bool use_mask = BWD ? G.mask_bwd : G.mask_fwd;
 
     // Owned states j = tid + k*T (k < SPT).  Slots with j ≥ K are inert: their
-    // part entry stays 0̄, pdf 0, never stored to HBM.
-    int pdfk[SPT];      // emission column
-    int distk[SPT];     // viability distance
+    // partial stays 0̄, pdf 0, never stored to HBM.
+    int pdfk[SPT];   // emission column
+    int distk[SPT];  // viability distance
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-        int j = tid + k * T;
-        pdfk[k] = 0; distk[k] = 0;
+        const int j = tid + k * T;
+        pdfk[k] = 0;
+        distk[k] = 0;
         if (j < K) {
             pdfk[k] = G.pdf[s0 + j];
             distk[k] = BWD ? G.dist_start[s0 + j] : G.dist_fin[s0 + j];
         }
-        sm.part[j] = NINF;  // rows without arcs are never written by phase A
+        sts_v(a_part + (uint32_t)j * VS, NINF);  // rows without arcs are never written by phase A
     }
     const float *em = a.emis + (size_t)b * a.N_max * a.D;
     const size_t lat_base = (size_t)a.N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
@@ -427,96 +440,115 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     auto load_alpha = [&](int n, float *v) {
         const float *row = a.alpha + lat_base + (size_t)min(max(n, 0), N - 1) * K;
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-            int j = tid + k * T;
-            v[k] = __ldg(row + min(j, K - 1));
-        }
+        for (int k = 0; k < SPT; ++k) v[k] = __ldg(row + min(tid + k * T, K - 1));
     };
     // viable(k, n): forward — a final state is reachable in the N-1-n remaining
     // transitions; backward — the state is reachable from an initial state in n.
     auto viable = [&](int k, int n) { return !use_mask || (BWD ? (distk[k] <= n) : (distk[k] <= N - 1 - n)); };
 
-    float vcur[SPT], vnxt[SPT];   // emissions of the frame being produced and the next one
-    float acur[SPT], anxt[SPT];   // α̂ prefetch (backward epilogue)
-    V cand[SPT], ucand[SPT];      // new α̂ / β̂ candidates and (bwd) v + β̂
-    V xpost[SPT];                 // α̂_n + β̂_n of the frame whose posterior is pending
+    float vcur[SPT], vnxt[SPT];  // emissions of the frame being produced and the next one
+    float acur[SPT], anxt[SPT];  // α̂ prefetch (backward epilogue)
+    V uk[SPT];                   // this thread's entries of the current vector u (log2)
+    V xpost[SPT];                // α̂_n + β̂_n of the frame whose posterior is pending
     const int dir = BWD ? -1 : 1;
     const int n_first = BWD ? N - 1 : 0;
     load_v(n_first, vcur);
     load_v(n_first + dir, vnxt);
     if (want_post) { load_alpha(n_first, acur); load_alpha(n_first + dir, anxt); }
-    double scale = 0.0;   // C_n (fwd) / D_n (bwd), log2 units
-    float vsum = 0.f;     // Σ of every emission read: NaN / +∞ ⇒ non-finite input
-    bool pend = false;    // a posterior row is pending (its Z in wz[parity])
-    int pend_n = 0;
+    double scale = 0.0;  // C_n (fwd) / D_n (bwd), log2 units
+    float vsum = 0.f;    // Σ of every emission read: NaN / +∞ ⇒ non-finite input
+    int par = 0;         // parity of the reduction buffers of the current frame
 
-    // ---- frame n_first: π ⊗ v_0 (fwd, L6) / β̂_{N-1} = ω (bwd, L7)
-    {
+    // Store frame n's normalised values h (α̂_n or β̂_n) and u; reduce max(u) and,
+    // in the backward, the log-sum-exp of x = α̂_n + β̂_n into buffers [par].
+    auto emit = [&](int n, const V *h) {
+        float *latn = a.lat ? a.lat + lat_base + (size_t)n * K : nullptr;
         V lmax = NINF;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
-            int j = tid + k * T;
-            bool ok = j < K && viable(k, n_first);
-            float v = vcur[k];
-            vsum += v;
-            V v2 = (V)v * L2E;
-            if (!BWD) {
-                cand[k] = ok ? (V)G.init2[s0 + min(j, K - 1)] + v2 : NINF;
-                lmax = vmax(lmax, cand[k]);
-            } else {
-                cand[k] = ok ? (V)G.final2[s0 + min(j, K - 1)] : NINF;
-                ucand[k] = cand[k] + v2;
-                lmax = vmax(lmax, ucand[k]);
-            }
+            const int j = tid + k * T;
+            if (j < K && latn) latn[j] = (float)(h[k] * LN2);
+            sts_v(a_u + (uint32_t)j * VS, uk[k]);
+            if (MODE == MODE_FACTORED) sts_v(a_p + (uint32_t)j * 4, ex2((float)uk[k]));
+            lmax = vmax(lmax, uk[k]);
         }
         lmax = warp_max(lmax);
-        if (lane == 0) sm.wmax[warp] = (double)lmax;
-    }
-    __syncthreads();  // schedule, wmax visible
-    int n = n_first;
-    for (int step = 0;; ++step) {
-        // ---- phase B2 of frame n: normalise, store, refresh u/p
-        {
-            V c = block_max_from<V>(sm.wmax + (step & 1) * 32, W, lane);
-            if (c == NINF) c = (V)0;  // no viable state: keep 0̄ everywhere
-            scale += (double)c;
-            if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
-            float *latn = a.lat ? a.lat + lat_base + (size_t)n * K : nullptr;
+        if (lane == 0) sts_v(a_wmax + (uint32_t)(par * 32 + warp) * 8, (double)lmax);
+        if (want_post) {
+            V zm = NINF;
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
-                int j = tid + k * T;
-                V h = cand[k] - c;   // α̂_n or β̂_n (log2)
-                V uu = BWD ? ucand[k] - c : h;
-                ucand[k] = uu;
-                if (j < K) {
-                    if (latn) latn[j] = (float)(h * LN2);
-                    sm.u[j] = uu;
-                    if (MODE == MODE_FACTORED) sm.p[j] = ex2((float)uu);
-                }
-                if (want_post) xpost[k] = (V)acur[k] * L2E + h;
+                xpost[k] = (tid + k * T < K) ? (V)acur[k] * L2E + h[k] : NINF;
+                zm = vmax(zm, xpost[k]);
             }
-            if (want_post) {
-                // block log-sum-exp of x = α̂_n + β̂_n (the per-frame normaliser Z_n)
-                V zm = NINF;
+            float zs = 0.f;
+            if (zm != NINF) {
 #pragma unroll
-                for (int k = 0; k < SPT; ++k) zm = vmax(zm, (tid + k * T < K) ? xpost[k] : NINF);
-                float zs = 0.f;
-                if (zm != NINF) {
-#pragma unroll
-                    for (int k = 0; k < SPT; ++k) zs += (tid + k * T < K) ? ex2((float)(xpost[k] - zm)) : 0.f;
-                }
-                warp_lse(zm, zs);
-                if (lane == 0) {
-                    sm.wz[(step & 1) * 64 + 2 * warp] = (double)zm;
-                    sm.wz[(step & 1) * 64 + 2 * warp + 1] = (double)zs;
-                }
+                for (int k = 0; k < SPT; ++k) zs += ex2((float)(xpost[k] - zm));
+            }
+            warp_lse(zm, zs);
+            if (lane == 0) {
+                sts_v(a_wz + (uint32_t)(par * 64 + 2 * warp) * 8, (double)zm);
+                sts_v(a_wz + (uint32_t)(par * 64 + 2 * warp + 1) * 8, (double)zs);
             }
         }
+    };
+    // γ of the frame whose x and Z (buffers [pp]) were produced one frame ago.
+    auto posterior = [&](int pn, int pp) {
+        V m = lane < W ? (V)lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane) * 8, 0.0) : NINF;
+        float s = lane < W ? (float)lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.0) : 0.f;
+        warp_lse(m, s);
+        const V Z = (m == NINF) ? NINF : m + (V)lg2(s);
+        float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pn * K : gbuf;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            const int j = tid + k * T;
+            const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
+            if (j < K) prow[j] = gam;
+        }
+    };
+    auto block_max_prev = [&](int pp) {
+        V v = lane < W ? (V)lds_v(a_wmax + (uint32_t)(pp * 32 + lane) * 8, 0.0) : NINF;
+        return warp_max(v);
+    };
+
+    // ---- first frame: π ⊗ v_0 (fwd, L6) / β̂_{N-1} = ω (bwd, L7), exact max
+    {
+        V h[SPT];
+        V lmax = NINF;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            const int j = tid + k * T;
+            const bool ok = j < K && viable(k, n_first);
+            const float v = vcur[k];
+            vsum += v;
+            const V v2 = (V)v * L2E;
+            if (!BWD) {
+                h[k] = ok ? (V)G.init2[s0 + min(j, K - 1)] + v2 : NINF;
+                uk[k] = h[k];
+            } else {
+                h[k] = ok ? (V)G.final2[s0 + min(j, K - 1)] : NINF;
+                uk[k] = h[k] + v2;
+            }
+            lmax = vmax(lmax, uk[k]);
+        }
+        lmax = warp_max(lmax);
+        if (lane == 0) sts_v(a_wmax + (uint32_t)(32 + warp) * 8, (double)lmax);
+        __syncthreads();  // schedule, flag, wmax[1] visible
+        V c = block_max_prev(1);
+        if (c == NINF) c = (V)0;
+        scale = (double)c;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) { h[k] -= c; uk[k] -= c; }
+        if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n_first] = scale * kLN2;
+        emit(n_first, h);
+    }
+    int n = n_first;
+    int pend_n = n_first;  // frame whose posterior is pending
+    for (;;) {
         const int n_next = n + dir;
-        const bool last = BWD ? (n_next < 0) : (n_next >= N);
-        __syncthreads();
-        if (want_post) { pend = true; pend_n = n; }
-        if (last) break;
+        if (BWD ? (n_next < 0) : (n_next >= N)) break;
+        __syncthreads();  // u, p, wmax[par], wz[par] of frame n visible
         // rotate prefetch: frame n_next becomes current, issue n_next + dir
 #pragma unroll
         for (int k = 0; k < SPT; ++k) vcur[k] = vnxt[k];
@@ -526,61 +558,48 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
             for (int k = 0; k < SPT; ++k) acur[k] = anxt[k];
             load_alpha(n_next + dir, anxt);
         }
+        // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
+        if (pdf_post && pend_n != n) pdf_row(a, gbuf, gi, b, pend_n, tid, T);
+        phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
+        __syncthreads();
+        // ---- phase B of frame n_next
+        const int pp = par;
+        par ^= 1;
+        if (want_post) posterior(n, pp);  // γ_n (its x is in registers, Z in wz[pp])
+        pend_n = n;
         n = n_next;
-        // ---- phase A of frame n
-        phase_a<MODE, V>(mysl, nsl, lane, sm.u, sm.p, sm.part);
-        __syncthreads();
-        // ---- phase B1 of frame n (+ pending posterior of frame n - dir)
-        {
-            V lmax = NINF;
-#pragma unroll
-            for (int k = 0; k < SPT; ++k) {
-                V y = sm.part[tid + k * T];
-                const bool ok = viable(k, n);
-                float v = vcur[k];
-                vsum += v;
-                V v2 = (V)v * L2E;
-                if (!BWD) {
-                    cand[k] = ok ? y + v2 : NINF;
-                    lmax = vmax(lmax, cand[k]);
-                } else {
-                    cand[k] = ok ? y : NINF;
-                    ucand[k] = cand[k] + v2;
-                    lmax = vmax(lmax, ucand[k]);
-                }
-            }
-            lmax = warp_max(lmax);
-            if (lane == 0) sm.wmax[((step + 1) & 1) * 32 + warp] = (double)lmax;
-            // γ of the pending frame; gbuf may alias part, so only after the reads above
-            if (pend) {
-                V Z = block_lse_from<V>(sm.wz + (step & 1) * 64, W, lane);
-                float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pend_n * K : sm.gbuf;
-#pragma unroll
-                for (int k = 0; k < SPT; ++k) {
-                    int j = tid + k * T;
-                    float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
-                    if (j < K) prow[j] = gam;
-                }
-            }
-        }
-        __syncthreads();
-        if (pdf_post && pend) pdf_row(a, sm.gbuf, gi, b, pend_n, tid, T);
-        pend = false;
-    }
-    // ---- flush the last pending posterior row (frame 0 in the backward).  The
-    // loop ran N B2 phases (steps 0..N-1), so its wz parity is (N-1) & 1.
-    const int lastpar = (N - 1) & 1;
-    if (want_post && pend) {
-        V Z = block_lse_from<V>(sm.wz + lastpar * 64, W, lane);
-        float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pend_n * K : sm.gbuf;
+        V c = block_max_prev(pp);         // lagged normaliser: max of the previous u
+        if (c == NINF) c = (V)0;          // no viable state: keep 0̄ everywhere
+        scale += (double)c;
+        if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
+        V h[SPT];
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
-            int j = tid + k * T;
-            float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
-            if (j < K) prow[j] = gam;
+            const V y = lds_v(a_part + (uint32_t)(tid + k * T) * VS, (V)0);
+            const bool ok = viable(k, n);
+            const float v = vcur[k];
+            vsum += v;
+            const V v2 = (V)v * L2E;
+            if (!BWD) {
+                h[k] = ok ? y + v2 - c : NINF;
+                uk[k] = h[k];
+            } else {
+                h[k] = ok ? y - c : NINF;
+                uk[k] = h[k] + v2;
+            }
         }
-        __syncthreads();
-        if (pdf_post) pdf_row(a, sm.gbuf, gi, b, pend_n, tid, T);
+        emit(n, h);
+    }
+    // ---- flush the pending posterior rows
+    if (want_post) {
+        __syncthreads();  // wz[par] of the last frame visible; gbuf of pend_n complete
+        if (pdf_post && pend_n != n) pdf_row(a, gbuf, gi, b, pend_n, tid, T);
+        if (pdf_post) __syncthreads();  // gbuf free again
+        posterior(n, par);
+        if (pdf_post) {
+            __syncthreads();
+            pdf_row(a, gbuf, gi, b, n, tid, T);
+        }
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
     {
@@ -588,23 +607,25 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         float zs = 0.f;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
-            int j = tid + k * T;
-            if (j < K) lse_push(zm, zs, ucand[k] + (V)(BWD ? G.init2[s0 + j] : G.final2[s0 + j]));
+            const int j = tid + k * T;
+            if (j < K) lse_push(zm, zs, uk[k] + (V)(BWD ? G.init2[s0 + j] : G.final2[s0 + j]));
         }
-        if (!(vsum < INFINITY)) sm.flag[0] = 1;
+        if (!(vsum < INFINITY)) sts_i(a_flag, 1);
         warp_lse(zm, zs);
-        __syncthreads();  // all readers of wz[lastpar] are done
+        __syncthreads();  // every reader of the reduction buffers is done
         if (lane == 0) {
-            sm.wz[(lastpar ^ 1) * 64 + 2 * warp] = (double)zm;
-            sm.wz[(lastpar ^ 1) * 64 + 2 * warp + 1] = (double)zs;
+            sts_v(a_wz + (uint32_t)(2 * warp) * 8, (double)zm);
+            sts_v(a_wz + (uint32_t)(2 * warp + 1) * 8, (double)zs);
         }
         __syncthreads();
         if (warp == 0) {
-            V m = block_lse_from<V>(sm.wz + (lastpar ^ 1) * 64, W, lane);
+            V m = lane < W ? (V)lds_v(a_wz + (uint32_t)(2 * lane) * 8, 0.0) : NINF;
+            float s = lane < W ? (float)lds_v(a_wz + (uint32_t)(2 * lane + 1) * 8, 0.0) : 0.f;
+            warp_lse(m, s);
             if (lane == 0) {
-                double z = (m == NINF) ? -INFINITY : (scale + (double)m) * kLN2;
+                double z = (m == NINF) ? -INFINITY : (scale + (double)m + (double)log2f(s)) * kLN2;
                 int stt = st;
-                if (sm.flag[0] == 1) stt |= FB_SEQ_NONFINITE_INPUT;
+                if (lds_i(a_flag) == 1) stt |= FB_SEQ_NONFINITE_INPUT;
                 if (!(z > -INFINITY)) stt |= FB_SEQ_EMPTY_LATTICE;
                 if (stt) z = -INFINITY;
                 if (a.logZ) a.logZ[b] = z;
@@ -736,8 +757,8 @@ static fb_status check_launch(const char *what) {
 
 static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s) {
     const Graph &G = a.g;
-    const bool post = bwd && a.post_kind != POST_NONE;
-    size_t sm = smem_bytes(G, bwd, post);
+    const bool post_pdf = bwd && a.post_kind != POST_NONE && a.post_kind != POST_STATE;
+    size_t sm = smem_bytes(G, bwd, post_pdf);
     KFn fn = pick(bwd, G.mode, G.spt, G.T);
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }

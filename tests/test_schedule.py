@@ -68,7 +68,7 @@ def decode(L, h, which, G, W, exact):
                 lg = (hdr[0] >> 16) & 7
                 L2 = int(np.uint32(hdr[0]) >> 19)
                 assert ((hdr >> 16) & 7 == lg).all() and (np.uint32(hdr) >> 19 == L2).all()  # uniform
-                idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint32).reshape(L2, 32)
+                idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint16).reshape(2 * L2, 32)
                 wt = blob[cur + 128 + L2 * 128:cur + 128 + L2 * 384].view(np.float32).reshape(L2, 32, 2)
                 gsz = 1 << lg
                 for lane in range(32):
@@ -79,8 +79,7 @@ def decode(L, h, which, G, W, exact):
                     arcs = []
                     for t in range(lane, lane + gsz):
                         for s in range(2 * L2):
-                            word = int(idx[s // 2, t])
-                            o = (word >> 16) if (s & 1) else (word & 0xFFFF)
+                            o = int(idx[s, t])
                             wv = float(wt[s // 2, t, s & 1])
                             if wv == pad:
                                 continue
