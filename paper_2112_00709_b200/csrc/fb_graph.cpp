@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <functional>
 #include <mutex>
 #include <new>
 #include <numeric>
@@ -109,38 +110,165 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     hs.blob.resize(off + bytes, 0);
     unsigned char *base = hs.blob.data() + off;
     const float padw = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
+    // shared-memory bank of a gathered element (32 banks of 4 bytes; an 8-byte
+    // element is treated as one of 16 double-width banks)
+    const int nbanks = esize == 4 ? 32 : 16;
+    auto bank_of = [&](uint32_t boff) { return (int)((boff / (uint32_t)esize) % (uint32_t)nbanks); };
+    std::vector<std::vector<long long>> rem(32);
     for (int w = 0; w < W; ++w) {
         size_t o = warp_off[w];
         for (int q : wsl[w]) {
             const Slice &s = sl[q];
             const int g = 1 << s.lg, L2 = s.L / 2;
             int32_t *hdr = (int32_t *)(base + o);
-            uint16_t *idx = (uint16_t *)(base + o + 128);
+            uint32_t *idx = (uint32_t *)(base + o + 128);
             float *wt = (float *)(base + o + 128 + (size_t)L2 * 128);
             for (int l = 0; l < 32; ++l) {
                 int ri = l >> s.lg, t = l & (g - 1);
                 bool has = ri < (int)s.rows.size();
                 uint32_t lead = (has && t == 0) ? (uint32_t)(s.rows[ri] + 1) : 0u;
                 hdr[l] = (int32_t)(lead | ((uint32_t)s.lg << 16) | ((uint32_t)L2 << 19));
-                long long a0 = 0, a1 = 0;
+                rem[l].clear();
                 if (has) {
                     const int r = s.rows[ri];
                     const long long d = rl.ptr[r + 1] - rl.ptr[r];
                     const long long len = (d + g - 1) / g;
-                    a0 = std::min<long long>(rl.ptr[r + 1], rl.ptr[r] + t * len);
-                    a1 = std::min<long long>(rl.ptr[r + 1], a0 + len);
+                    const long long a0 = std::min<long long>(rl.ptr[r + 1], rl.ptr[r] + t * len);
+                    const long long a1 = std::min<long long>(rl.ptr[r + 1], a0 + len);
+                    for (long long a = a0; a < a1; ++a) rem[l].push_back(a);
                 }
-                for (int sl2 = 0; sl2 < s.L; ++sl2) {
-                    long long a = a0 + sl2;
-                    uint32_t boff = 0;
+            }
+            // Bank-aware slot assignment.  A lane's arcs may run in any order (a
+            // fixed one, so results stay deterministic).  An arc-row costs as many
+            // shared-memory wavefronts as the most distinct addresses falling in one
+            // bank, so slots are assigned by bipartite edge colouring of the
+            // (lane, bank) multigraph with L colours (Kempe-chain flips, König):
+            // conflict-free whenever no bank carries more than L arcs of the slice;
+            // excess arcs take a colour free at their lane.  Null slots finally copy
+            // a live lane's address (a free broadcast).
+            const int Ls = s.L;
+            std::vector<long long> grid((size_t)Ls * 32, -1);  // arc index or -1 (null)
+            auto addr_of = [&](long long arc) { return (uint32_t)rl.other[arc] * (uint32_t)esize; };
+            {
+                // grid[c*32 + l] = arc of lane l in colour (slot) c; bank_c[b*Ls + c] =
+                // lane whose arc of bank b has colour c (proper edges only)
+                std::vector<int> bank_c((size_t)nbanks * Ls, -1);
+                std::vector<char> over((size_t)Ls * 32, 0);
+                auto G_ = [&](int l, int c) -> long long & { return grid[(size_t)c * 32 + l]; };
+                auto free_lane = [&](int l) {
+                    for (int c = 0; c < Ls; ++c) if (G_(l, c) < 0) return c;
+                    return -1;
+                };
+                auto free_bank = [&](int bk) {
+                    for (int c = 0; c < Ls; ++c) if (bank_c[(size_t)bk * Ls + c] < 0) return c;
+                    return -1;
+                };
+                size_t maxlen = 0;
+                for (int l = 0; l < 32; ++l) maxlen = std::max(maxlen, rem[l].size());
+                for (size_t c0 = 0; c0 < maxlen; ++c0)
+                    for (int l = 0; l < 32; ++l) {
+                        if (c0 >= rem[l].size()) continue;
+                        const long long arc = rem[l][c0];
+                        const int bk = bank_of(addr_of(arc));
+                        const int ca = free_lane(l);
+                        const int cb = free_bank(bk);
+                        bool placed = false;
+                        if (cb >= 0) {
+                            if (bank_c[(size_t)bk * Ls + ca] < 0) {
+                                placed = true;
+                            } else {
+                                // alternating (ca, cb) path from bank bk: bank -ca- lane -cb- bank ...
+                                std::vector<std::pair<int, int>> path;  // (lane, colour)
+                                bool ok = true;
+                                int vb = bk;
+                                while (true) {
+                                    const int ln = bank_c[(size_t)vb * Ls + ca];
+                                    if (ln < 0) break;
+                                    path.push_back({ln, ca});
+                                    const long long nx = G_(ln, cb);
+                                    if (nx < 0) break;
+                                    if (over[(size_t)cb * 32 + ln]) { ok = false; break; }
+                                    path.push_back({ln, cb});
+                                    vb = bank_of(addr_of(nx));
+                                }
+                                if (ok) {
+                                    std::vector<long long> arcs(path.size());
+                                    for (size_t i = 0; i < path.size(); ++i) {
+                                        arcs[i] = G_(path[i].first, path[i].second);
+                                        G_(path[i].first, path[i].second) = -1;
+                                        bank_c[(size_t)bank_of(addr_of(arcs[i])) * Ls + path[i].second] = -1;
+                                    }
+                                    for (size_t i = 0; i < path.size(); ++i) {
+                                        const int nc = path[i].second == ca ? cb : ca;
+                                        G_(path[i].first, nc) = arcs[i];
+                                        bank_c[(size_t)bank_of(addr_of(arcs[i])) * Ls + nc] = path[i].first;
+                                    }
+                                    placed = G_(l, ca) < 0 && bank_c[(size_t)bk * Ls + ca] < 0;
+                                }
+                            }
+                        }
+                        if (placed) {
+                            G_(l, ca) = arc;
+                            bank_c[(size_t)bk * Ls + ca] = l;
+                        } else {  // bank saturated (or blocked path): conflicting placement
+                            const int cx = free_lane(l);
+                            G_(l, cx) = arc;
+                            over[(size_t)cx * 32 + l] = 1;
+                        }
+                    }
+            }
+            // local search on top of the colouring: swap two slots of one lane when
+            // the two arc-rows' summed wavefront count does not grow (seeded, so the
+            // schedule is deterministic)
+            auto row_cost = [&](int r) {
+                uint32_t seen[32];
+                int ns = 0, cnt[32] = {0}, worst = 1;
+                for (int l = 0; l < 32; ++l) {
+                    const long long arc = grid[(size_t)r * 32 + l];
+                    if (arc < 0) continue;
+                    const uint32_t ad = addr_of(arc);
+                    bool dup = false;
+                    for (int x = 0; x < ns; ++x)
+                        if (seen[x] == ad) { dup = true; break; }
+                    if (dup) continue;
+                    seen[ns++] = ad;
+                    worst = std::max(worst, ++cnt[bank_of(ad)]);
+                }
+                return worst;
+            };
+            if (Ls > 1 && mode == MODE_FACTORED) {
+                std::vector<int> rc(Ls);
+                for (int r = 0; r < Ls; ++r) rc[r] = row_cost(r);
+                uint64_t rng = 0x9E3779B97F4A7C15ull ^ ((uint64_t)q << 17) ^ (uint64_t)Ls;
+                auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
+                const int iters = 60 * Ls * 32;
+                for (int it = 0; it < iters; ++it) {
+                    const int l = (int)(next() % 32), r1 = (int)(next() % Ls), r2 = (int)(next() % Ls);
+                    if (r1 == r2) continue;
+                    long long &x1 = grid[(size_t)r1 * 32 + l], &x2 = grid[(size_t)r2 * 32 + l];
+                    if (x1 < 0 && x2 < 0) continue;
+                    std::swap(x1, x2);
+                    const int c1 = row_cost(r1), c2 = row_cost(r2);
+                    if (c1 + c2 <= rc[r1] + rc[r2]) { rc[r1] = c1; rc[r2] = c2; }
+                    else std::swap(x1, x2);
+                }
+            }
+            for (int sl2 = 0; sl2 < Ls; ++sl2) {
+                uint32_t bcast = 0;
+                for (int l = 0; l < 32; ++l)
+                    if (grid[(size_t)sl2 * 32 + l] >= 0) { bcast = addr_of(grid[(size_t)sl2 * 32 + l]); break; }
+                for (int l = 0; l < 32; ++l) {
+                    const long long a = grid[(size_t)sl2 * 32 + l];
+                    uint32_t boff = bcast;
                     float wf = padw;
-                    if (a < a1) {
-                        boff = (uint32_t)rl.other[a] * (uint32_t)esize;
+                    if (a >= 0) {
+                        boff = addr_of(a);
                         double wn = rl.w[a];
                         wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
                         if (std::isinf(wn) && wn < 0) wf = padw;
                     }
-                    idx[sl2 * 32 + l] = (uint16_t)boff;
+                    uint32_t &word = idx[(sl2 / 2) * 32 + l];
+                    word |= (sl2 & 1) ? (boff << 16) : boff;
                     wt[((sl2 / 2) * 32 + l) * 2 + (sl2 & 1)] = wf;
                 }
             }

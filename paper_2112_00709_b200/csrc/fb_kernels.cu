@@ -214,7 +214,8 @@ __device__ __noinline__ float exact_row(uint32_t cur, int L2, int g, int lane, u
     float m = NEG_INF, sum = 0.f;
     for (int t = 0; t < g; ++t)
         for (int s = 0; s < 2 * L2; ++s) {
-            uint32_t o = lds_u16(cur + 128 + s * 64 + (lane + t) * 2);
+            uint32_t ix = lds_u32(cur + 128 + (s >> 1) * 128 + (lane + t) * 4);
+            uint32_t o = (s & 1) ? (ix >> 16) : (ix & 0xFFFFu);
             float w = lds_v(cur + 128 + L2 * 128 + (s >> 1) * 256 + (lane + t) * 8 + (s & 1) * 4, 0.f);
             float x = lds_v(a_u + o, 0.f) + log2f(w);
             if (x == NEG_INF) continue;
@@ -240,15 +241,15 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
     for (int q = 0; q < nsl; ++q) {
         const uint32_t h = lds_u32(cur + lane * 4);
         const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
-        uint32_t ia = cur + 128 + lane * 2;
+        uint32_t ia = cur + 128 + lane * 4;
         uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
         if (MODE == MODE_FACTORED) {
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll 2
             for (int s = 0; s < L2; ++s) {
-                const uint32_t o0 = lds_u16(ia), o1 = lds_u16(ia + 64);
+                const uint32_t ix = lds_u32(ia);
                 const float2 w2 = lds_f2(wa);
-                const float p0 = lds_v(a_p + o0, 0.f), p1 = lds_v(a_p + o1, 0.f);
+                const float p0 = lds_v(a_p + (ix & 0xFFFFu), 0.f), p1 = lds_v(a_p + (ix >> 16), 0.f);
                 a0 = fmaf(p0, w2.x, a0);
                 a1 = fmaf(p1, w2.y, a1);
                 ia += 128;
@@ -272,10 +273,10 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
                 m = hi;
             };
             for (int s = 0; s < L2; ++s) {
-                const uint32_t o0 = lds_u16(ia), o1 = lds_u16(ia + 64);
+                const uint32_t ix = lds_u32(ia);
                 const float2 w2 = lds_f2(wa);
-                push(m0, s0, o0, w2.x);
-                push(m1, s1, o1, w2.y);
+                push(m0, s0, ix & 0xFFFFu, w2.x);
+                push(m1, s1, ix >> 16, w2.y);
                 ia += 128;
                 wa += 256;
             }

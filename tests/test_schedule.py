@@ -68,7 +68,7 @@ def decode(L, h, which, G, W, exact):
                 lg = (hdr[0] >> 16) & 7
                 L2 = int(np.uint32(hdr[0]) >> 19)
                 assert ((hdr >> 16) & 7 == lg).all() and (np.uint32(hdr) >> 19 == L2).all()  # uniform
-                idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint16).reshape(2 * L2, 32)
+                idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint32).reshape(L2, 32)
                 wt = blob[cur + 128 + L2 * 128:cur + 128 + L2 * 384].view(np.float32).reshape(L2, 32, 2)
                 gsz = 1 << lg
                 for lane in range(32):
@@ -79,7 +79,8 @@ def decode(L, h, which, G, W, exact):
                     arcs = []
                     for t in range(lane, lane + gsz):
                         for s in range(2 * L2):
-                            o = int(idx[s, t])
+                            word = int(idx[s // 2, t])
+                            o = (word >> 16) if (s & 1) else (word & 0xFFFF)
                             wv = float(wt[s // 2, t, s & 1])
                             if wv == pad:
                                 continue
@@ -159,3 +160,30 @@ def test_hub_rows_split_across_lanes(L):
     g = synth.graph_from_arcs(K, src, dst, rng.uniform(-3, 0, len(src)), np.zeros(K), np.zeros(K))
     check_graph(L, g, flags=2)
     check_graph(L, g, flags=1)
+
+
+def test_bank_conflicts_reduced(L):
+    """Gathers of one arc-row should mostly hit distinct shared-memory banks."""
+    den = synth.make_den(3)
+    code, h, info = compile_dry(L, den)
+    n = L.fbx_debug_schedule(h, 0, None, None)
+    blob = np.zeros(n, np.uint8)
+    L.fbx_debug_schedule(h, 0, blob.ctypes.data_as(ctypes.c_void_p), None)
+    m = L.fbx_debug_schedule_meta_len(h, 0)
+    meta = np.zeros(m, np.int32)
+    L.fbx_debug_schedule(h, 0, None, meta.ctypes.data_as(ctypes.c_void_p))
+    W = int(info[4]) // 32
+    tot = rows = 0
+    for w in range(W):
+        cur, nsl = meta[2 + 2 * w], meta[2 + 2 * w + 1]
+        for _ in range(nsl):
+            L2 = int(np.uint32(blob[cur:cur + 4].view(np.int32)[0]) >> 19)
+            idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint32).reshape(L2, 32)
+            for half in (idx & 0xFFFF, idx >> 16):
+                for r in half:
+                    # wavefronts = most distinct addresses in one bank (equal addresses broadcast)
+                    banks = Counter((a // 4) % 32 for a in set(r.tolist()))
+                    tot += max(banks.values())
+                    rows += 1
+            cur += 128 + L2 * 384
+    assert tot / rows < 2.1, tot / rows  # unordered placement averages ~2.6-way
