@@ -120,6 +120,44 @@ __device__ __forceinline__ V warp_max(V v) {
     for (int o = 16; o; o >>= 1) v = vmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
+// Warp max of a float via one REDUX on order-preserving integer keys
+// (doubles use shuffles); warp sum via shuffles.
+__device__ __forceinline__ int f2key(float f) {
+    const int i = __float_as_int(f);
+    return i ^ ((i >> 31) & 0x7FFFFFFF);
+}
+__device__ __forceinline__ float key2f(int k) { return __int_as_float(k ^ ((k >> 31) & 0x7FFFFFFF)); }
+__device__ __forceinline__ float warp_max_fast(float v) { return key2f(__reduce_max_sync(0xffffffffu, f2key(v))); }
+__device__ __forceinline__ double warp_max_fast(double v) { return warp_max(v); }
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+// Block log-sum-exp (log2) from per-warp (max, Σ 2^{x-max}) pairs held by lanes < W.
+template <class V>
+__device__ __forceinline__ V block_lse_pairs(V m, float s) {
+    const V M = warp_max_fast(m);
+    const V Ms = (M == ninf<V>()) ? (V)0 : M;
+    const float t = (m == ninf<V>()) ? 0.f : s * ex2((float)(m - Ms));
+    const float S = warp_sum(t);
+    return (M == ninf<V>()) ? M : M + (V)lg2(S);
+}
+// This thread's (max, Σ) over its SPT values reduced over the warp.
+template <class V, int SPT>
+__device__ __forceinline__ void warp_lse_vals(const V *x, V &wm, float &ws) {
+    V m = ninf<V>();
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) m = vmax(m, x[k]);
+    m = warp_max_fast(m);
+    const V ms = (m == ninf<V>()) ? (V)0 : m;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) s += ex2((float)(x[k] - ms));
+    wm = m;
+    ws = warp_sum(s);
+}
+
 // (m, s) log-sum-exp pair (value = m + log2 s), m in V, s in float (s ∈ [1, n])
 template <class V>
 __device__ __forceinline__ void lse_push(V &m, float &s, V x) {
@@ -473,44 +511,37 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
             if (MODE == MODE_FACTORED) sts_v(a_p + (uint32_t)j * 4, ex2((float)uk[k]));
             lmax = vmax(lmax, uk[k]);
         }
-        lmax = warp_max(lmax);
-        if (lane == 0) sts_v(a_wmax + (uint32_t)(par * 32 + warp) * 8, (double)lmax);
+        lmax = warp_max_fast(lmax);
+        if (lane == 0) sts_v(a_wmax + (uint32_t)(par * 32 + warp) * 8, lmax);
         if (want_post) {
-            V zm = NINF;
 #pragma unroll
-            for (int k = 0; k < SPT; ++k) {
-                xpost[k] = (tid + k * T < K) ? (V)acur[k] * L2E + h[k] : NINF;
-                zm = vmax(zm, xpost[k]);
-            }
-            float zs = 0.f;
-            if (zm != NINF) {
-#pragma unroll
-                for (int k = 0; k < SPT; ++k) zs += ex2((float)(xpost[k] - zm));
-            }
-            warp_lse(zm, zs);
+            for (int k = 0; k < SPT; ++k) xpost[k] = (tid + k * T < K) ? (V)acur[k] * L2E + h[k] : NINF;
+            V zm;
+            float zs;
+            warp_lse_vals<V, SPT>(xpost, zm, zs);
             if (lane == 0) {
-                sts_v(a_wz + (uint32_t)(par * 64 + 2 * warp) * 8, (double)zm);
-                sts_v(a_wz + (uint32_t)(par * 64 + 2 * warp + 1) * 8, (double)zs);
+                sts_v(a_wz + (uint32_t)(par * 64 + 2 * warp) * 8, zm);
+                sts_v(a_wz + (uint32_t)(par * 64 + 2 * warp + 1) * 8, zs);
             }
         }
     };
     // γ of the frame whose x and Z (buffers [pp]) were produced one frame ago.
     auto posterior = [&](int pn, int pp) {
-        V m = lane < W ? (V)lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane) * 8, 0.0) : NINF;
-        float s = lane < W ? (float)lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.0) : 0.f;
-        warp_lse(m, s);
-        const V Z = (m == NINF) ? NINF : m + (V)lg2(s);
+        const V m = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane) * 8, (V)0) : NINF;
+        const float s = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
+        const V Z = block_lse_pairs<V>(m, s);
+        const V Zs = (Z == NINF) ? (V)0 : Z;
         float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pn * K : gbuf;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int j = tid + k * T;
-            const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Z));
+            const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Zs));
             if (j < K) prow[j] = gam;
         }
     };
     auto block_max_prev = [&](int pp) {
-        V v = lane < W ? (V)lds_v(a_wmax + (uint32_t)(pp * 32 + lane) * 8, 0.0) : NINF;
-        return warp_max(v);
+        const V v = lane < W ? lds_v(a_wmax + (uint32_t)(pp * 32 + lane) * 8, (V)0) : NINF;
+        return warp_max_fast(v);
     };
 
     // ---- first frame: π ⊗ v_0 (fwd, L6) / β̂_{N-1} = ω (bwd, L7), exact max
@@ -533,8 +564,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
             }
             lmax = vmax(lmax, uk[k]);
         }
-        lmax = warp_max(lmax);
-        if (lane == 0) sts_v(a_wmax + (uint32_t)(32 + warp) * 8, (double)lmax);
+        lmax = warp_max_fast(lmax);
+        if (lane == 0) sts_v(a_wmax + (uint32_t)(32 + warp) * 8, lmax);
         __syncthreads();  // schedule, flag, wmax[1] visible
         V c = block_max_prev(1);
         if (c == NINF) c = (V)0;
@@ -604,27 +635,33 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
     {
-        V zm = NINF;
-        float zs = 0.f;
+        V xt[SPT];
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int j = tid + k * T;
-            if (j < K) lse_push(zm, zs, uk[k] + (V)(BWD ? G.init2[s0 + j] : G.final2[s0 + j]));
+            xt[k] = (j < K) ? uk[k] + (V)(BWD ? G.init2[s0 + j] : G.final2[s0 + j]) : NINF;
         }
+        V zm;
+        float zs;
+        warp_lse_vals<V, SPT>(xt, zm, zs);
         if (!(vsum < INFINITY)) sts_i(a_flag, 1);
-        warp_lse(zm, zs);
         __syncthreads();  // every reader of the reduction buffers is done
         if (lane == 0) {
-            sts_v(a_wz + (uint32_t)(2 * warp) * 8, (double)zm);
-            sts_v(a_wz + (uint32_t)(2 * warp + 1) * 8, (double)zs);
+            sts_v(a_wz + (uint32_t)(2 * warp) * 8, zm);
+            sts_v(a_wz + (uint32_t)(2 * warp + 1) * 8, zs);
         }
         __syncthreads();
         if (warp == 0) {
-            V m = lane < W ? (V)lds_v(a_wz + (uint32_t)(2 * lane) * 8, 0.0) : NINF;
-            float s = lane < W ? (float)lds_v(a_wz + (uint32_t)(2 * lane + 1) * 8, 0.0) : 0.f;
-            warp_lse(m, s);
+            const V m = lane < W ? lds_v(a_wz + (uint32_t)(2 * lane) * 8, (V)0) : NINF;
+            const float sx = lane < W ? lds_v(a_wz + (uint32_t)(2 * lane + 1) * 8, 0.f) : 0.f;
+            // float64 final combine of the per-warp pairs (logZ is assembled in fp64)
+            const V M = warp_max_fast(m);
+            const double Md = (M == NINF) ? 0.0 : (double)M;
+            double t = (m == NINF) ? 0.0 : (double)sx * exp2((double)m - Md);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
             if (lane == 0) {
-                double z = (m == NINF) ? -INFINITY : (scale + (double)m + (double)log2f(s)) * kLN2;
+                double z = (M == NINF) ? -INFINITY : (scale + Md + log2(t)) * kLN2;
                 int stt = st;
                 if (lds_i(a_flag) == 1) stt |= FB_SEQ_NONFINITE_INPUT;
                 if (!(z > -INFINITY)) stt |= FB_SEQ_EMPTY_LATTICE;
