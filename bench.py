@@ -1,0 +1,322 @@
+"""bench.py — LF-MMI loss+gradient throughput on B200 (BASELINE.json metric).
+
+Metric: forward-backward frames×seqs/sec on the denominator graph, B = 128
+utterances per GPU (weak scaling), measured as the whole hot path of SURVEY §8(a):
+numerator + denominator forward-backward, posteriors, LF-MMI gradient, loss and
+totals (+ NCCL all-reduce of the 5 totals when N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (SURVEY §8(d) C4, configs[3]): den K=3000 / nnz=20000 (2% hub skew),
+pdf map 3000→2000, 128 numerator graphs (L ~ U[50,150] phones), φ [128,500,2000]
+U[-10,0) fp32, all N_b = 500; rank r draws its own batch (seed 4 + 1000 r).
+Inputs (φ 512 MB, grad 512 MB, α̂ 768 MB per step) exceed the 126 MB L2.
+
+The reference arm (--impl reference) is the float64 C oracle (oracle/) run on
+this host's cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+B, N, D, K_DEN, NNZ_DEN = 128, 500, 2000, 3000, 20000
+METRIC = "forward-backward frames×seqs/sec (den graph, B=128) & % HBM roofline @1/2/4/8 GPU"
+WORKLOAD = "C4: LF-MMI loss+grad, den K=3000 nnz=20000 (pdf 3000→2000) + 128 numerator graphs, φ[128,500,2000] fp32 per GPU"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_batch(rank: int):
+    from paper_2112_00709_b200 import synth
+
+    w = synth.make_c4(seed=4, B=B, N=N, K=K_DEN, nnz=NNZ_DEN, D=D)
+    if rank:
+        # rank r: same denominator graph, its own numerator graphs and emissions
+        rng = np.random.Generator(np.random.PCG64(4 + 1000 * rank))
+        w.nums = [synth.numerator_graph(rng, int(rng.integers(50, 151)), D, "random") for _ in range(B)]
+        w.emis = synth.emissions(rng, B, N, D)
+    return w
+
+
+# ---------------------------------------------------------------------------- reference arm
+
+def cpu_oracle_rate(w, n_utts: int, threads: int):
+    """Oracle seq-frames/s on the first n_utts utterances of the batch."""
+    import oracle
+    from paper_2112_00709_b200 import synth
+
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    oracle.lib()
+    num = synth.compose(w.nums[:n_utts])
+    den = synth.compose([w.den])
+    t0 = time.perf_counter()
+    r = oracle.lfmmi_batch(num, den, w.emis[:n_utts], w.lengths[:n_utts])
+    dt = time.perf_counter() - t0
+    assert (r["status"] == 0).all()
+    return float(w.lengths[:n_utts].sum()) / dt, dt
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    w = make_batch(0)
+    per_step = max(1, min(B, threads))
+    sample = f"{per_step} of the 128 C4 utterances per step (full length 500), float64 oracle, OpenMP over utterances"
+    times = []
+    for i in range(args.warmup + args.steps):
+        lo = (i * per_step) % B
+        sub = type(w)(w.name, per_step, N, D, w.lengths[lo:lo + per_step], w.emis[lo:lo + per_step], den=w.den,
+                      nums=w.nums[lo:lo + per_step])
+        _, dt = cpu_oracle_rate(sub, per_step, threads)
+        if i >= args.warmup:
+            times.append(dt)
+    frames = per_step * N
+    value = frames * len(times) / sum(times)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "seq-frames/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD + " (sampled)", "global_batch": per_step, "seq_len": N,
+                       "parallelism": "cpu-openmp"},
+            "cpu_baseline": {"value": value, "unit": "seq-frames/s", "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "seq-frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2112_00709_b200 as fbx
+    from paper_2112_00709_b200 import build, synth
+
+    build.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    t0 = time.time()
+    w = make_batch(rank)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    log(f"[rank {rank}] inputs ready in {time.time() - t0:.1f}s; den {den.info} num K_tot {num.K_tot}")
+    emis = torch.from_numpy(w.emis).to(dev)
+    lens = torch.from_numpy(w.lengths).to(dev)
+    grad = torch.empty_like(emis)
+    ws = torch.empty(fbx.workspace_bytes(num, den, B, N), dtype=torch.uint8, device=dev)
+    loss = torch.empty(B, dtype=torch.float64, device=dev)
+    totals = torch.empty(5, dtype=torch.float64, device=dev)
+    status = torch.empty(B, dtype=torch.int32, device=dev)
+
+    def step():
+        fbx.lfmmi_loss_grad(num, den, emis, lens, grad, ws, loss, totals, status)
+        if world > 1:
+            dist.all_reduce(totals)  # NCCL on the current stream: Σ loss, Σ frames, Σ logZ, n_bad
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    st_host = status.cpu().numpy()
+    assert (st_host == 0).all(), st_host
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    fbx.profile_reset()
+    fbx.profile_enable(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            step()
+        ev1.record()
+        torch.cuda.synchronize()
+    fbx.profile_enable(False)
+    prof = fbx.profile_collect()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    frames_total = float(w.lengths.sum()) * world * args.steps
+    value = frames_total / (ms / 1e3)
+
+    # per-kernel roofline (dominant kernel: the denominator backward with the fused gradient epilogue)
+    hbm, peak_src = measured_peaks()
+    seq_frames = float(w.lengths.sum())
+    alg_bytes = {  # algorithmic bytes per launch
+        "k_fb_bwd[G=1]": seq_frames * (4 * D + 4 * K_DEN + 4 * D),  # φ row, α̂ row, grad row
+        "k_fb_fwd[G=1]": seq_frames * (4 * D + 4 * K_DEN),  # φ row, α̂ row
+    }
+    kern = {}
+    for name, (cnt, tot_ms) in prof.items():
+        avg = tot_ms / max(cnt, 1)
+        kern[name] = {"launches": cnt, "avg_ms": avg}
+        if name in alg_bytes:
+            kern[name]["achieved_gbs"] = alg_bytes[name] / (avg / 1e3) / 1e9
+    dom = "k_fb_bwd[G=1]"
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get(dom)
+    achieved = kern.get(dom, {}).get("achieved_gbs")
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": alg_bytes[dom]}
+    step_bytes = alg_bytes["k_fb_bwd[G=1]"] + alg_bytes["k_fb_fwd[G=1]"]
+    launches = sum(c for c, _ in prof.values())
+
+    # end to end through the public API with host buffers (pinned φ in, totals + loss out)
+    e2e = None
+    if rank == 0 or world > 1:
+        emis_h = torch.from_numpy(w.emis).pin_memory()
+        lens_h = torch.from_numpy(w.lengths)
+        bufs = {}
+        for _ in range(2):
+            fbx.lfmmi_loss_grad_host(num, den, emis_h, lens_h, bufs)
+        torch.cuda.synchronize()
+        k2 = max(3, min(args.steps, 10))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k2):
+            out = fbx.lfmmi_loss_grad_host(num, den, emis_h, lens_h, bufs)
+            if world > 1:
+                dist.all_reduce(bufs["totals"])
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": seq_frames * world * k2 / (ems / 1e3), "unit": "seq-frames/s",
+               "h2d_bytes_per_step": int(emis_h.numel() * 4 + lens_h.numel() * 4),
+               "d2h_bytes_per_step": int(out.numel() * 8), "steps": k2}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        n_utts = max(1, min(B, 2 * threads))
+        rate, dt = cpu_oracle_rate(w, n_utts, threads)
+        cpu = {"value": rate, "unit": "seq-frames/s", "cores": threads, "kind": "oracle",
+               "sample": f"{n_utts} of the 128 C4 utterances at full length (500 frames), "
+                         f"float64 C oracle, {dt:.1f} s wall"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "seq-frames/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY §8(d) C4 recipe)",
+        "config": {"workload": WORKLOAD, "global_batch": B * world, "seq_len": N, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (φ 512 MB, grad 512 MB, α̂ 768 MB per step)"},
+        "hbm_fraction_of_step": (step_bytes / (ms / args.steps / 1e3) / 1e9) / hbm,
+        "roofline": roofline, "kernels": kern, "gpu_launches": launches, "clocks": clk.summary(),
+        "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()
