@@ -402,6 +402,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     std::vector<int> dist_fin(K_tot, kFar), dist_start(K_tot, kFar);
     std::vector<int> slot_off(G + 1, 0), slot_pdf, slot_sptr(1, 0), slot_states;
     std::vector<int> pdf_slot((size_t)G * D, -1);
+    std::vector<int> slot_pos(K_tot, 0);
     std::vector<float> init2(K_tot), final2(K_tot);
     for (int i = 0; i < K_tot; ++i) {
         init2[i] = (float)((double)log_init[i] * kLog2e);
@@ -473,6 +474,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
                 slot_pdf.push_back(ps[x].first);
                 pdf_slot[(size_t)g * D + ps[x].first] = local++;
             }
+            slot_pos[s0 + ps[x].second] = (int)(slot_states.size() - (size_t)slot_sptr[slot_off[g]]);
             slot_states.push_back(ps[x].second);
         }
         slot_sptr.push_back((int)slot_states.size());
@@ -489,7 +491,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
     gr.bwd.bytes_max = hb.bytes_max; gr.bwd.slots_max = hb.slots_max;
     gr.pm.U_tot = slot_off[G];
-    if (smem_bytes(gr, false, false) > (size_t)kSmemLimit || smem_bytes(gr, true, true) > (size_t)kSmemLimit)
+    if (gr.pm.U_max >= 32768 || (long long)D * 2 > 65536) return FB_ERR_UNSUPPORTED;  // i16 pdf maps in smem
+    if (smem_bytes(gr, false, false) > (size_t)kSmemLimit ||
+        smem_bytes(gr, true, true) + pdf_region(POST_GRAD, gr.pm.U_max, D, gr.pm.U_max).bytes > (size_t)kSmemLimit)
         return FB_ERR_UNSUPPORTED;
 
     // pack and upload
@@ -506,7 +510,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     };
     SO of = put_sched(hf), ob = put_sched(hb);
     size_t o_so = pk.put(slot_off), o_spd = pk.put(slot_pdf), o_ssp = pk.put(slot_sptr),
-           o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot);
+           o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot), o_spo = pk.put(slot_pos);
     if (flags & FB_GRAPH_DRY_RUN) {
         fb_graph h = new (std::nothrow) fb_graph_s;
         if (!h) return FB_ERR_NOMEM;
@@ -548,6 +552,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.pm.slot_off = (const int *)P(o_so); gr.pm.slot_pdf = (const int *)P(o_spd);
     gr.pm.slot_sptr = (const int *)P(o_ssp); gr.pm.slot_states = (const int *)P(o_sst);
     gr.pm.pdf_slot = (const int *)P(o_pds);
+    gr.pm.slot_pos = (const int *)P(o_spo);
     fb_graph h = new (std::nothrow) fb_graph_s;
     if (!h) { cudaFree(dev); return FB_ERR_NOMEM; }
     h->g = gr;

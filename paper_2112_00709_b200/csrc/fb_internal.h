@@ -54,6 +54,7 @@ struct PdfMap {
     const int *slot_sptr = nullptr;
     const int *slot_states = nullptr;
     const int *pdf_slot = nullptr;
+    const int *slot_pos = nullptr;    // [K_tot] position of a state in its member's slot-ordered list
     int U_max = 0;
     long long U_tot = 0;
 };
@@ -105,6 +106,28 @@ FBX_HD inline SmemLayout smem_layout(int rec_bytes, int K_pad, bool exact, bool 
     L.red = o; o += fbx_a16(8 * (2 * 32 + 2 * 64) + 64);
     L.total = o;
     return L;
+}
+
+// Output kinds of the backward posterior epilogue.
+enum PostKind : int { POST_NONE = 0, POST_STATE = 1, POST_PDF_DENSE = 2, POST_PDF_COMPACT = 3, POST_GRAD = 4 };
+
+// Shared-memory region of the pdf-level epilogue, placed after the reductions:
+// ssp   u16[U+1]  slot boundaries of the member's slot-ordered state list
+// pslot i16[D]    pdf → slot (-1 unused)            (dense / grad)
+// nslot i16[D]    pdf → numerator slot (-1 unused)  (grad)
+// gnbuf f32[Un]   one row of numerator pdf posteriors (grad)
+struct PdfRegion {
+    size_t ssp, pslot, nslot, gnbuf, bytes;
+};
+FBX_HD inline PdfRegion pdf_region(int kind, int U_max, int D, int num_U_max) {
+    PdfRegion R;
+    size_t o = 0;
+    R.ssp = o; o += fbx_a16((size_t)(U_max + 1) * 2);
+    R.pslot = o; if (kind == POST_PDF_DENSE || kind == POST_GRAD) o += fbx_a16((size_t)D * 2);
+    R.nslot = o; if (kind == POST_GRAD) o += fbx_a16((size_t)D * 2);
+    R.gnbuf = o; if (kind == POST_GRAD) o += fbx_a16((size_t)(num_U_max > 0 ? num_U_max : 1) * 4);
+    R.bytes = (kind == POST_PDF_DENSE || kind == POST_PDF_COMPACT || kind == POST_GRAD) ? o : 0;
+    return R;
 }
 
 // Dynamic shared memory needed by a forward/backward launch over this graph.

@@ -222,8 +222,6 @@ __device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
     return m == ninf<V>() ? ninf<V>() : m + (V)lg2(s);
 }
 
-// Output kinds of the backward posterior epilogue.
-enum PostKind : int { POST_NONE = 0, POST_STATE = 1, POST_PDF_DENSE = 2, POST_PDF_COMPACT = 3, POST_GRAD = 4 };
 
 struct FBArgs {
     Graph g;
@@ -243,6 +241,7 @@ struct FBArgs {
     const float *gnum;
     const int *num_slot_off;
     const int *num_pdf_slot; // [B*D]
+    int num_U_max;           // largest numerator slot count (gnbuf size)
 };
 
 // Exact max-then-sum over one row held by g lanes (fallback of factored mode,
@@ -330,41 +329,34 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
     }
 }
 
-// Write one frame's pdf-level posterior (or gradient) row from gbuf.
-__device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, int gi, int b, int n, int tid, int T) {
+// Write one frame's pdf-level posterior (or gradient) row.  gbuf holds γ in the
+// member's slot order, so pdf slot s sums gbuf[ssp[s] .. ssp[s+1]) (ascending
+// state order, ledger L9); maps staged in shared memory (PdfRegion).
+__device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, const unsigned short *ssp,
+                                        const short *pslot, const short *nslot, const float *gnbuf, int gi, int b,
+                                        int n, int tid, int T) {
     const Graph &G = a.g;
     const PdfMap &pm = G.pm;
-    const int D = a.D;
     if (a.post_kind == POST_PDF_COMPACT) {
         const int so = pm.slot_off[gi], U = pm.slot_off[gi + 1] - so;
         float *row = a.post + (size_t)a.N_max * so + (size_t)n * U;
         for (int sl = tid; sl < U; sl += T) {
             float acc = 0.f;
-            for (int q = pm.slot_sptr[so + sl]; q < pm.slot_sptr[so + sl + 1]; ++q) acc += gbuf[pm.slot_states[q]];
+            for (int q = ssp[sl]; q < ssp[sl + 1]; ++q) acc += gbuf[q];
             row[sl] = acc;
         }
         return;
     }
-    const int so = pm.slot_off[gi];
+    const int D = a.D;
     float *row = a.post + ((size_t)b * a.N_max + n) * D;
-    const int *ps = pm.pdf_slot + (size_t)gi * D;
-    const float *gn = nullptr;
-    const int *nps = nullptr;
-    if (a.post_kind == POST_GRAD) {
-        const int nso = a.num_slot_off[b];
-        const int nU = a.num_slot_off[b + 1] - nso;
-        gn = a.gnum + (size_t)a.N_max * nso + (size_t)n * nU;
-        nps = a.num_pdf_slot + (size_t)b * D;
-    }
     for (int d = tid; d < D; d += T) {
-        int sl = __ldg(ps + d);
+        const int sl = pslot[d];
         float acc = 0.f;
         if (sl >= 0)
-            for (int q = pm.slot_sptr[so + sl]; q < pm.slot_sptr[so + sl + 1]; ++q) acc += gbuf[pm.slot_states[q]];
+            for (int q = ssp[sl]; q < ssp[sl + 1]; ++q) acc += gbuf[q];
         if (a.post_kind == POST_GRAD) {
-            int ns = __ldg(nps + d);
-            float g = ns >= 0 ? gn[ns] : 0.f;
-            row[d] = g - acc;
+            const int ns = nslot[d];
+            row[d] = (ns >= 0 ? gnbuf[ns] : 0.f) - acc;
         } else {
             row[d] = acc;
         }
@@ -421,6 +413,11 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     const uint32_t a_u = sb + (uint32_t)SL.u, a_p = sb + (uint32_t)SL.p, a_part = sb + (uint32_t)SL.part;
     const uint32_t a_wmax = sb + (uint32_t)SL.red, a_wz = a_wmax + 64 * 8, a_flag = a_wmax + 192 * 8;
     float *gbuf = (float *)(smem_raw + SL.gbuf);
+    const PdfRegion PR = pdf_region(a.post_kind, G.pm.U_max, a.D, a.num_U_max);
+    unsigned short *ssp = (unsigned short *)(smem_raw + SL.total + PR.ssp);
+    short *pslot = (short *)(smem_raw + SL.total + PR.pslot);
+    short *nslot = (short *)(smem_raw + SL.total + PR.nslot);
+    float *gnbuf = (float *)(smem_raw + SL.total + PR.gnbuf);
     const V L2E = (V)1.4426950408889634;
     const V LN2 = (V)0.6931471805599453;
     const V NINF = ninf<V>();
@@ -450,6 +447,22 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         for (int x = tid; x < n16; x += T) dst[x] = src[x];
     }
     if (tid == 0) sts_i(a_flag, 0);
+    // pdf-level epilogue maps → shared memory
+    int nU = 0;                    // numerator slots of this utterance (grad)
+    const float *gnrow0 = nullptr; // numerator Γ rows of this utterance (grad)
+    if (pdf_post) {
+        const int so = G.pm.slot_off[gi], U = G.pm.slot_off[gi + 1] - so;
+        const int base = G.pm.slot_sptr[so];
+        for (int x = tid; x <= U; x += T) ssp[x] = (unsigned short)(G.pm.slot_sptr[so + x] - base);
+        if (a.post_kind != POST_PDF_COMPACT)
+            for (int d = tid; d < a.D; d += T) pslot[d] = (short)G.pm.pdf_slot[(size_t)gi * a.D + d];
+        if (a.post_kind == POST_GRAD) {
+            for (int d = tid; d < a.D; d += T) nslot[d] = (short)a.num_pdf_slot[(size_t)b * a.D + d];
+            const int nso = a.num_slot_off[b];
+            nU = a.num_slot_off[b + 1] - nso;
+            gnrow0 = a.gnum + (size_t)a.N_max * nso;
+        }
+    }
     const int nsl = S.warp_nsl[gi * W + warp];
     const uint32_t mysl = sb + (uint32_t)SL.rec + (uint32_t)S.warp_off[gi * W + warp];
     const bool use_mask = BWD ? G.mask_bwd : G.mask_fwd;
@@ -458,14 +471,17 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     // partial stays 0̄, pdf 0, never stored to HBM.
     int pdfk[SPT];   // emission column
     int distk[SPT];  // viability distance
+    int posk[SPT];   // position in the slot-ordered γ buffer (pdf-level epilogue)
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
         const int j = tid + k * T;
         pdfk[k] = 0;
         distk[k] = 0;
+        posk[k] = 0;
         if (j < K) {
             pdfk[k] = G.pdf[s0 + j];
             distk[k] = BWD ? G.dist_start[s0 + j] : G.dist_fin[s0 + j];
+            if (pdf_post) posk[k] = G.pm.slot_pos[s0 + j];
         }
         sts_v(a_part + (uint32_t)j * VS, NINF);  // rows without arcs are never written by phase A
     }
@@ -485,6 +501,12 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     // transitions; backward — the state is reachable from an initial state in n.
     auto viable = [&](int k, int n) { return !use_mask || (BWD ? (distk[k] <= n) : (distk[k] <= N - 1 - n)); };
 
+    // numerator Γ row values (grad epilogue): gq_a for the next posterior row, gq_b the one after
+    auto load_gn = [&](int n) {
+        return (tid < nU) ? __ldg(gnrow0 + (size_t)min(max(n, 0), N - 1) * nU + tid) : 0.f;
+    };
+    float gq_a = 0.f, gq_b = 0.f;
+    if (a.post_kind == POST_GRAD) { gq_a = load_gn(N - 1); gq_b = load_gn(N - 2); }
     float vcur[SPT], vnxt[SPT];  // emissions of the frame being produced and the next one
     float acur[SPT], anxt[SPT];  // α̂ prefetch (backward epilogue)
     V uk[SPT];                   // this thread's entries of the current vector u (log2)
@@ -531,12 +553,19 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         const float s = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
         const V Z = block_lse_pairs<V>(m, s);
         const V Zs = (Z == NINF) ? (V)0 : Z;
-        float *prow = a.post_kind == POST_STATE ? a.post + lat_base + (size_t)pn * K : gbuf;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int j = tid + k * T;
             const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Zs));
-            if (j < K) prow[j] = gam;
+            if (j < K) {
+                if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pn * K + j] = gam;
+                else gbuf[posk[k]] = gam;
+            }
+        }
+        if (a.post_kind == POST_GRAD) {  // numerator Γ row of frame pn (prefetched two frames ago)
+            if (tid < nU) gnbuf[tid] = gq_a;
+            gq_a = gq_b;
+            gq_b = load_gn(pn + 2 * dir);
         }
     };
     auto block_max_prev = [&](int pp) {
@@ -591,7 +620,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
             load_alpha(n_next + dir, anxt);
         }
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
-        if (pdf_post && pend_n != n) pdf_row(a, gbuf, gi, b, pend_n, tid, T);
+        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, nslot, gnbuf, gi, b, pend_n, tid, T);
         phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
         __syncthreads();
         // ---- phase B of frame n_next
@@ -625,12 +654,12 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     // ---- flush the pending posterior rows
     if (want_post) {
         __syncthreads();  // wz[par] of the last frame visible; gbuf of pend_n complete
-        if (pdf_post && pend_n != n) pdf_row(a, gbuf, gi, b, pend_n, tid, T);
+        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, nslot, gnbuf, gi, b, pend_n, tid, T);
         if (pdf_post) __syncthreads();  // gbuf free again
         posterior(n, par);
         if (pdf_post) {
             __syncthreads();
-            pdf_row(a, gbuf, gi, b, n, tid, T);
+            pdf_row(a, gbuf, ssp, pslot, nslot, gnbuf, gi, b, n, tid, T);
         }
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
@@ -796,7 +825,7 @@ static fb_status check_launch(const char *what) {
 static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s) {
     const Graph &G = a.g;
     const bool post_pdf = bwd && a.post_kind != POST_NONE && a.post_kind != POST_STATE;
-    size_t sm = smem_bytes(G, bwd, post_pdf);
+    size_t sm = smem_bytes(G, bwd, post_pdf) + (post_pdf ? pdf_region(a.post_kind, G.pm.U_max, a.D, a.num_U_max).bytes : 0);
     KFn fn = pick(bwd, G.mode, G.spt, G.T);
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
@@ -964,6 +993,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
         c.status = seq_status; c.status2 = nst; c.alpha = den_alpha;
         c.post = grad; c.post_kind = POST_GRAD;
         c.gnum = gnum; c.num_slot_off = num->g.pm.slot_off; c.num_pdf_slot = num->g.pm.pdf_slot;
+        c.num_U_max = num->g.pm.U_max;
         if ((r = launch_fb(true, c, s)) != FB_OK) return r;
     }
     {
