@@ -553,13 +553,19 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         const float s = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
         const V Z = block_lse_pairs<V>(m, s);
         const V Zs = (Z == NINF) ? (V)0 : Z;
+        if (a.post_kind == POST_STATE) {
+            float *prow = a.post + lat_base + (size_t)pn * K;
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-            const int j = tid + k * T;
-            const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Zs));
-            if (j < K) {
-                if (a.post_kind == POST_STATE) a.post[lat_base + (size_t)pn * K + j] = gam;
-                else gbuf[posk[k]] = gam;
+            for (int k = 0; k < SPT; ++k) {
+                const int j = tid + k * T;
+                const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Zs));
+                if (j < K) prow[j] = gam;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Zs));
+                if (tid + k * T < K) gbuf[posk[k]] = gam;
             }
         }
         if (a.post_kind == POST_GRAD) {  // numerator Γ row of frame pn (prefetched two frames ago)
@@ -968,14 +974,16 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     cudaStream_t s = (cudaStream_t)stream;
     SideRes *sr = side_res();
     fb_status r;
-    // denominator forward first: its B CTAs each take a whole SM (registers and
-    // shared memory), so the numerator CTAs forked next land on the idle SMs.
+    // The fork point is recorded before the denominator forward so the numerator
+    // pass depends only on prior work; the denominator forward is submitted first:
+    // its B CTAs each take a whole SM (registers and shared memory), so the
+    // numerator CTAs land on the SMs it leaves idle and the two run concurrently.
+    cudaEventRecord(sr->fork, s);
     {
         FBArgs a = base_args(den, log_emis, lengths, B, N_max);
         a.lat = den_alpha; a.logZ = zd; a.status = seq_status;
         if ((r = launch_fb(false, a, s)) != FB_OK) return r;
     }
-    cudaEventRecord(sr->fork, s);
     cudaStreamWaitEvent(sr->s, sr->fork, 0);
     {
         FBArgs a = base_args(num, log_emis, lengths, B, N_max);
