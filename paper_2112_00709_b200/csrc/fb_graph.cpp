@@ -264,7 +264,8 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
                     if (a >= 0) {
                         boff = addr_of(a);
                         double wn = rl.w[a];
-                        wf = (mode == MODE_FACTORED) ? (float)std::exp(wn) : (float)(wn * kLog2e);
+                        wf = (mode == MODE_FACTORED) ? (float)std::exp(wn)
+                             : (mode == MODE_VITERBI) ? (float)wn : (float)(wn * kLog2e);
                         if (std::isinf(wn) && wn < 0) wf = padw;
                     }
                     uint32_t &word = idx[(sl2 / 2) * 32 + l];
@@ -306,6 +307,10 @@ struct Packer {
 bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
 
 }  // namespace
+
+size_t viterbi_smem_bytes(const Graph &g) {
+    return smem_layout(g.vit.bytes_max, g.T * g.spt, true, false).total + fbx_a16((size_t)g.T * g.spt * 4);
+}
 
 size_t smem_bytes(const Graph &g, bool backward, bool post) {
     const Sched &s = backward ? g.bwd : g.fwd;
@@ -398,7 +403,8 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.spt = spt;
 
     // per-member schedules, distances, pdf slots
-    HostSched hf, hb;
+    HostSched hf, hb, hv;
+    bool vit_ok = true;
     std::vector<int> dist_fin(K_tot, kFar), dist_start(K_tot, kFar);
     std::vector<int> slot_off(G + 1, 0), slot_pdf, slot_sptr(1, 0), slot_states;
     std::vector<int> pdf_slot((size_t)G * D, -1);
@@ -441,6 +447,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         const int esize = gr.mode == MODE_EXACT ? 8 : 4;
         if (!build_member_sched(in, K, T, gr.mode, esize, lmax, hf)) return FB_ERR_UNSUPPORTED;
         if (!build_member_sched(outl, K, T, gr.mode, esize, lmax, hb)) return FB_ERR_UNSUPPORTED;
+        if (vit_ok && !build_member_sched(in, K, T, MODE_VITERBI, 8, lmax, hv)) vit_ok = false;
         // BFS over finite arcs: distance to a final state (reverse) / from an initial state
         std::deque<int> q;
         for (int k = 0; k < K; ++k)
@@ -490,6 +497,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     // mode, u in exact mode), which the kernel addresses as [offset + base]
     gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
     gr.bwd.bytes_max = hb.bytes_max; gr.bwd.slots_max = hb.slots_max;
+    gr.vit.bytes_max = hv.bytes_max; gr.vit.slots_max = hv.slots_max;
+    gr.vit_ok = vit_ok && viterbi_smem_bytes(gr) <= (size_t)kSmemLimit;
+    if (!gr.vit_ok) hv = HostSched();
     gr.pm.U_tot = slot_off[G];
     if (gr.pm.U_max >= 32768 || (long long)D * 2 > 65536) return FB_ERR_UNSUPPORTED;  // i16 pdf maps in smem
     if (smem_bytes(gr, false, false) > (size_t)kSmemLimit ||
@@ -501,6 +511,8 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     std::vector<int> soff(state_offsets, state_offsets + G + 1);
     size_t o_soff = pk.put(soff), o_pdf = pk.put(pdf), o_i2 = pk.put(init2), o_f2 = pk.put(final2);
     size_t o_df = pk.put(dist_fin), o_ds = pk.put(dist_start);
+    std::vector<float> init_nat(log_init, log_init + K_tot), final_nat(log_final, log_final + K_tot);
+    size_t o_in = pk.put(init_nat), o_fn = pk.put(final_nat);
     struct SO { size_t rec, rb, ro, wo, wn; };
     auto put_sched = [&](HostSched &h) {
         SO o;
@@ -508,7 +520,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         o.wn = pk.put(h.warp_nsl);
         return o;
     };
-    SO of = put_sched(hf), ob = put_sched(hb);
+    SO of = put_sched(hf), ob = put_sched(hb), ov = put_sched(hv);
     size_t o_so = pk.put(slot_off), o_spd = pk.put(slot_pdf), o_ssp = pk.put(slot_sptr),
            o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot), o_spo = pk.put(slot_pos);
     if (flags & FB_GRAPH_DRY_RUN) {
@@ -543,12 +555,15 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.final2 = (const float *)P(o_f2);
     gr.dist_fin = (const int *)P(o_df);
     gr.dist_start = (const int *)P(o_ds);
+    gr.init_nat = (const float *)P(o_in);
+    gr.final_nat = (const float *)P(o_fn);
     auto set_sched = [&](Sched &d, const SO &o) {
         d.rec = (const unsigned char *)P(o.rec); d.rec_bytes = (const int *)P(o.rb);
         d.rec_off = (const long long *)P(o.ro); d.warp_off = (const int *)P(o.wo); d.warp_nsl = (const int *)P(o.wn);
     };
     set_sched(gr.fwd, of);
     set_sched(gr.bwd, ob);
+    set_sched(gr.vit, ov);
     gr.pm.slot_off = (const int *)P(o_so); gr.pm.slot_pdf = (const int *)P(o_spd);
     gr.pm.slot_sptr = (const int *)P(o_ssp); gr.pm.slot_states = (const int *)P(o_sst);
     gr.pm.pdf_slot = (const int *)P(o_pds);

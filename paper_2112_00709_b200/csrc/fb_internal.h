@@ -15,7 +15,9 @@ constexpr int kMaxSPT = 8;          // states per thread held in registers
 constexpr int kMaxThreads = 1024;   // threads per CTA (one CTA per sequence)
 constexpr int kSmemLimit = 227 * 1024;
 
-enum Mode : int { MODE_FACTORED = 0, MODE_EXACT = 1 };
+enum Mode : int { MODE_FACTORED = 0, MODE_EXACT = 1,
+                  MODE_RAW = 2,       // exact arithmetic, float64 lattices, no per-frame normalisation (lfmmi numerator)
+                  MODE_VITERBI = 3 }; // schedule encoding of the tropical pass: natural-log weights, float64 gathers
 
 // One direction's arc schedule in grouped sliced-ELL form (forward = in-arcs /
 // CSC of T, backward = out-arcs / CSR; ledger L3).  A row (the state being
@@ -70,9 +72,13 @@ struct Graph {
     const int *pdf = nullptr;         // [K_tot]
     const float *init2 = nullptr;     // [K_tot] π · log2(e)
     const float *final2 = nullptr;    // [K_tot] ω · log2(e)
+    const float *init_nat = nullptr;  // [K_tot] π (natural log, as given)
+    const float *final_nat = nullptr; // [K_tot] ω (natural log, as given)
     const int *dist_fin = nullptr;    // [K_tot] min #transitions to a final state (INT_MAX/2 if none)
     const int *dist_start = nullptr;  // [K_tot] min #transitions from an initial state
     Sched fwd, bwd;
+    Sched vit;        // forward (in-arc) schedule with natural-log weights for fb_viterbi
+    int vit_ok = 0;   // the Viterbi schedule fits shared memory
     PdfMap pm;
     void *block = nullptr;
     size_t block_bytes = 0;
@@ -132,6 +138,8 @@ FBX_HD inline PdfRegion pdf_region(int kind, int U_max, int D, int num_U_max) {
 
 // Dynamic shared memory needed by a forward/backward launch over this graph.
 size_t smem_bytes(const Graph &g, bool backward, bool pdf_level);
+// ... and by a Viterbi launch (float64 u / best, int32 arg per state).
+size_t viterbi_smem_bytes(const Graph &g);
 
 }  // namespace fbx
 

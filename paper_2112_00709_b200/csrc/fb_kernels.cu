@@ -242,6 +242,10 @@ struct FBArgs {
     const int *num_slot_off;
     const int *num_pdf_slot; // [B*D]
     int num_U_max;           // largest numerator slot count (gnbuf size)
+    // MODE_RAW (lfmmi numerator): float64 log2 lattices, posteriors normalised by logZ_in
+    double *lat64;
+    const double *alpha64;
+    const double *logZ_in;
 };
 
 // Exact max-then-sum over one row held by g lanes (fallback of factored mode,
@@ -395,8 +399,9 @@ __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, in
 // in range (exact fallback otherwise).
 template <bool BWD, int MODE, int SPT, int MAXT>
 __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArgs a) {
-    using V = typename std::conditional<MODE == MODE_EXACT, double, float>::type;
+    using V = typename std::conditional<MODE == MODE_FACTORED, float, double>::type;
     constexpr uint32_t VS = sizeof(V);
+    constexpr bool RAW = MODE == MODE_RAW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Graph &G = a.g;
     const int b = blockIdx.x;
@@ -408,7 +413,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     const Sched &S = BWD ? G.bwd : G.fwd;
     const bool want_post = BWD && a.post_kind != POST_NONE;
     const bool pdf_post = want_post && a.post_kind != POST_STATE;
-    const SmemLayout SL = smem_layout(S.bytes_max, T * SPT, MODE == MODE_EXACT, want_post && pdf_post);
+    const SmemLayout SL = smem_layout(S.bytes_max, T * SPT, MODE != MODE_FACTORED, want_post && pdf_post);
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t a_u = sb + (uint32_t)SL.u, a_p = sb + (uint32_t)SL.p, a_part = sb + (uint32_t)SL.part;
     const uint32_t a_wmax = sb + (uint32_t)SL.red, a_wz = a_wmax + 64 * 8, a_flag = a_wmax + 192 * 8;
@@ -492,10 +497,15 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
 #pragma unroll
         for (int k = 0; k < SPT; ++k) v[k] = __ldg(row + pdfk[k]);
     };
-    auto load_alpha = [&](int n, float *v) {
-        const float *row = a.alpha + lat_base + (size_t)min(max(n, 0), N - 1) * K;
+    // α̂ of frame n in log2 units (float natural-log lattice, or the raw float64 log2 one)
+    auto load_alpha = [&](int n, V *v) {
+        const size_t ro = lat_base + (size_t)min(max(n, 0), N - 1) * K;
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) v[k] = __ldg(row + min(tid + k * T, K - 1));
+        for (int k = 0; k < SPT; ++k) {
+            const int j = min(tid + k * T, K - 1);
+            if (RAW) v[k] = (V)__ldg(a.alpha64 + ro + j);
+            else v[k] = (V)__ldg(a.alpha + ro + j) * L2E;
+        }
     };
     // viable(k, n): forward — a final state is reachable in the N-1-n remaining
     // transitions; backward — the state is reachable from an initial state in n.
@@ -508,7 +518,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     float gq_a = 0.f, gq_b = 0.f;
     if (a.post_kind == POST_GRAD) { gq_a = load_gn(N - 1); gq_b = load_gn(N - 2); }
     float vcur[SPT], vnxt[SPT];  // emissions of the frame being produced and the next one
-    float acur[SPT], anxt[SPT];  // α̂ prefetch (backward epilogue)
+    V acur[SPT], anxt[SPT];      // α̂ prefetch (backward epilogue), log2 units
     V uk[SPT];                   // this thread's entries of the current vector u (log2)
     V xpost[SPT];                // α̂_n + β̂_n of the frame whose posterior is pending
     const int dir = BWD ? -1 : 1;
@@ -523,21 +533,27 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     // Store frame n's normalised values h (α̂_n or β̂_n) and u; reduce max(u) and,
     // in the backward, the log-sum-exp of x = α̂_n + β̂_n into buffers [par].
     auto emit = [&](int n, const V *h) {
-        float *latn = a.lat ? a.lat + lat_base + (size_t)n * K : nullptr;
+        float *latn = (!RAW && a.lat) ? a.lat + lat_base + (size_t)n * K : nullptr;
+        double *latn64 = (RAW && a.lat64) ? a.lat64 + lat_base + (size_t)n * K : nullptr;
         V lmax = NINF;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int j = tid + k * T;
             if (j < K && latn) latn[j] = (float)(h[k] * LN2);
+            if (j < K && latn64) latn64[j] = (double)h[k];
             sts_v(a_u + (uint32_t)j * VS, uk[k]);
             if (MODE == MODE_FACTORED) sts_v(a_p + (uint32_t)j * 4, ex2((float)uk[k]));
             lmax = vmax(lmax, uk[k]);
         }
-        lmax = warp_max_fast(lmax);
-        if (lane == 0) sts_v(a_wmax + (uint32_t)(par * 32 + warp) * 8, lmax);
+        if (!RAW) {
+            lmax = warp_max_fast(lmax);
+            if (lane == 0) sts_v(a_wmax + (uint32_t)(par * 32 + warp) * 8, lmax);
+        }
         if (want_post) {
 #pragma unroll
-            for (int k = 0; k < SPT; ++k) xpost[k] = (tid + k * T < K) ? (V)acur[k] * L2E + h[k] : NINF;
+            for (int k = 0; k < SPT; ++k) xpost[k] = (tid + k * T < K) ? acur[k] + h[k] : NINF;
+        }
+        if (want_post && !RAW) {
             V zm;
             float zs;
             warp_lse_vals<V, SPT>(xpost, zm, zs);
@@ -549,9 +565,15 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
     };
     // γ of the frame whose x and Z (buffers [pp]) were produced one frame ago.
     auto posterior = [&](int pn, int pp) {
-        const V m = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane) * 8, (V)0) : NINF;
-        const float s = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
-        const V Z = block_lse_pairs<V>(m, s);
+        V Z;
+        if (RAW) {  // unnormalised float64 lattices: Eq. (15) with the forward's logZ
+            const double z = a.logZ_in[b];
+            Z = (z > -INFINITY) ? (V)(z * 1.4426950408889634) : NINF;
+        } else {
+            const V m = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane) * 8, (V)0) : NINF;
+            const float s = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
+            Z = block_lse_pairs<V>(m, s);
+        }
         const V Zs = (Z == NINF) ? (V)0 : Z;
         if (a.post_kind == POST_STATE) {
             float *prow = a.post + lat_base + (size_t)pn * K;
@@ -599,10 +621,12 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
             }
             lmax = vmax(lmax, uk[k]);
         }
-        lmax = warp_max_fast(lmax);
-        if (lane == 0) sts_v(a_wmax + (uint32_t)(32 + warp) * 8, lmax);
+        if (!RAW) {
+            lmax = warp_max_fast(lmax);
+            if (lane == 0) sts_v(a_wmax + (uint32_t)(32 + warp) * 8, lmax);
+        }
         __syncthreads();  // schedule, flag, wmax[1] visible
-        V c = block_max_prev(1);
+        V c = RAW ? (V)0 : block_max_prev(1);
         if (c == NINF) c = (V)0;
         scale = (double)c;
 #pragma unroll
@@ -635,8 +659,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
         if (want_post) posterior(n, pp);  // γ_n (its x is in registers, Z in wz[pp])
         pend_n = n;
         n = n_next;
-        V c = block_max_prev(pp);         // lagged normaliser: max of the previous u
-        if (c == NINF) c = (V)0;          // no viable state: keep 0̄ everywhere
+        V c = RAW ? (V)0 : block_max_prev(pp);  // lagged normaliser: max of the previous u
+        if (c == NINF) c = (V)0;                // no viable state: keep 0̄ everywhere
         scale += (double)c;
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
         V h[SPT];
@@ -703,6 +727,178 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArg
                 if (stt) z = -INFINITY;
                 if (a.logZ) a.logZ[b] = z;
                 a.status[b] = stt;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ Viterbi (tropical semiring, N1)
+
+// Max-plus phase A over the Viterbi schedule (natural-log weights, float64
+// gathers): per row, the best predecessor score and its source (lowest index
+// on ties, the oracle's rule).
+__device__ __forceinline__ void vit_consider(double &best, int &arg, double x, int src) {
+    if (x > best || (x == best && src < arg)) { best = x; arg = src; }
+}
+
+__device__ __forceinline__ void phase_a_max(uint32_t cur, int nsl, int lane, uint32_t a_u, uint32_t a_best,
+                                            uint32_t a_arg) {
+    for (int q = 0; q < nsl; ++q) {
+        const uint32_t h = lds_u32(cur + lane * 4);
+        const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
+        uint32_t ia = cur + 128 + lane * 4;
+        uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
+        double b0 = NEG_INF_D, b1 = NEG_INF_D;
+        int g0 = 0x7fffffff, g1 = 0x7fffffff;
+        for (int s = 0; s < L2; ++s) {
+            const uint32_t ix = lds_u32(ia);
+            const float2 w2 = lds_f2(wa);
+            const uint32_t o0 = ix & 0xFFFFu, o1 = ix >> 16;
+            vit_consider(b0, g0, lds_v(a_u + o0, 0.0) + (double)w2.x, (int)(o0 >> 3));
+            vit_consider(b1, g1, lds_v(a_u + o1, 0.0) + (double)w2.y, (int)(o1 >> 3));
+            ia += 128;
+            wa += 256;
+        }
+        vit_consider(b0, g0, b1, g1);
+        for (int o = 1; o < (1 << lg); o <<= 1) {
+            const double bo = __shfl_xor_sync(0xffffffffu, b0, o);
+            const int go = __shfl_xor_sync(0xffffffffu, g0, o);
+            vit_consider(b0, g0, bo, go);
+        }
+        if (row >= 0) {
+            sts_v(a_best + (uint32_t)row * 8, b0);
+            sts_i(a_arg + (uint32_t)row * 4, b0 == NEG_INF_D ? -1 : g0);
+        }
+        cur += 128 + (uint32_t)L2 * 384;
+    }
+}
+
+struct VitArgs {
+    Graph g;
+    const float *emis;
+    const int *lengths;
+    int B, N_max, D;
+    double *score;  // [B]
+    int *path;      // [B][N_max]
+    int *status;    // [B]
+    void *bp;       // backpointers [B][N_max][K] (int16 if K ≤ 32767 else int32)
+    int bp16;
+};
+
+// One CTA per sequence: δ_0 = π ⊗ v_0; δ_n(j) = v_n(j) ⊗ max_{i→j} δ_{n-1}(i) ⊗ T_ij
+// (Eq. (13) with ⊕ = max), backpointers to HBM, argmax of δ_{N-1} ⊗ ω,
+// backtrace by one thread.  Float64 values, no normalisation: scores are the
+// same float64 sums the oracle forms, so the tie-broken path agrees exactly.
+template <int SPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const VitArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Graph &G = a.g;
+    const Sched &S = G.vit;
+    const int b = blockIdx.x;
+    const int gi = (G.G == 1) ? 0 : b;
+    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
+    const int s0 = G.state_off[gi];
+    const int K = G.state_off[gi + 1] - s0;
+    const int N = a.lengths[b];
+    const SmemLayout SL = smem_layout(S.bytes_max, T * SPT, true, false);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t a_u = sb + (uint32_t)SL.u, a_best = sb + (uint32_t)SL.part;
+    const uint32_t a_red = sb + (uint32_t)SL.red, a_arg = sb + (uint32_t)SL.total;
+    int *path = a.path + (size_t)b * a.N_max;
+    for (int n = max(0, min(N, a.N_max)) + tid; n < a.N_max; n += T) path[n] = -1;
+    if (N < 1 || N > a.N_max) {
+        for (int n = tid; n < a.N_max; n += T) path[n] = -1;
+        if (tid == 0) { a.score[b] = -INFINITY; a.status[b] = FB_SEQ_BAD_LENGTH; }
+        return;
+    }
+    {
+        const uint4 *src = (const uint4 *)(S.rec + S.rec_off[gi]);
+        uint4 *dst = (uint4 *)(smem_raw + SL.rec);
+        const int n16 = S.rec_bytes[gi] >> 4;
+        for (int x = tid; x < n16; x += T) dst[x] = src[x];
+    }
+    const int nsl = S.warp_nsl[gi * W + warp];
+    const uint32_t mysl = sb + (uint32_t)SL.rec + (uint32_t)S.warp_off[gi * W + warp];
+    int pdfk[SPT];
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+        const int j = tid + k * T;
+        pdfk[k] = j < K ? G.pdf[s0 + j] : 0;
+        sts_v(a_best + (uint32_t)j * 8, NEG_INF_D);
+    }
+    const float *em = a.emis + (size_t)b * a.N_max * a.D;
+    const size_t bp_base = (size_t)b * a.N_max * G.K_max;  // [B][N_max][K_max]
+    float vsum = 0.f;
+    double dk[SPT];
+    // frame 0 (natural log, float64: the same sums the oracle forms)
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+        const int j = tid + k * T;
+        const float v = __ldg(em + pdfk[k]);
+        vsum += j < K ? v : 0.f;
+        dk[k] = j < K ? (double)G.init_nat[s0 + j] + (double)v : NEG_INF_D;
+        sts_v(a_u + (uint32_t)j * 8, dk[k]);
+    }
+    for (int n = 1; n < N; ++n) {
+        __syncthreads();
+        phase_a_max(mysl, nsl, lane, a_u, a_best, a_arg);
+        __syncthreads();
+        const float *row = em + (size_t)n * a.D;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            const int j = tid + k * T;
+            const double best = lds_v(a_best + (uint32_t)j * 8, 0.0);
+            const float v = __ldg(row + pdfk[k]);
+            vsum += j < K ? v : 0.f;
+            dk[k] = (best == NEG_INF_D) ? NEG_INF_D : best + (double)v;
+            sts_v(a_u + (uint32_t)j * 8, dk[k]);
+            if (j < K) {
+                const int arg = lds_i(a_arg + (uint32_t)j * 4);
+                if (a.bp16) ((short *)a.bp)[bp_base + (size_t)n * K + j] = (short)arg;
+                else ((int *)a.bp)[bp_base + (size_t)n * K + j] = arg;
+            }
+        }
+    }
+    // argmax_j δ_{N-1}(j) ⊗ ω(j), lowest index on ties
+    double best = NEG_INF_D;
+    int arg = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+        const int j = tid + k * T;
+        if (j < K) vit_consider(best, arg, dk[k] + (double)G.final_nat[s0 + j], j);
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double bo = __shfl_xor_sync(0xffffffffu, best, o);
+        const int go = __shfl_xor_sync(0xffffffffu, arg, o);
+        vit_consider(best, arg, bo, go);
+    }
+    // barrier (phase-A buffers free, this CTA's backpointers visible) + non-finite vote
+    const int bad = __syncthreads_or(!(vsum < INFINITY));
+    if (lane == 0) {
+        sts_v(a_red + (uint32_t)warp * 16, best);
+        sts_i(a_red + (uint32_t)warp * 16 + 8, arg);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        best = lane < W ? lds_v(a_red + (uint32_t)lane * 16, 0.0) : NEG_INF_D;
+        arg = lane < W ? lds_i(a_red + (uint32_t)lane * 16 + 8) : 0x7fffffff;
+        for (int o = 16; o; o >>= 1) {
+            const double bo = __shfl_xor_sync(0xffffffffu, best, o);
+            const int go = __shfl_xor_sync(0xffffffffu, arg, o);
+            vit_consider(best, arg, bo, go);
+        }
+        if (lane == 0) {
+            int st = 0;
+            if (bad) st |= FB_SEQ_NONFINITE_INPUT;
+            if (best == NEG_INF_D) st |= FB_SEQ_EMPTY_LATTICE;
+            a.score[b] = st ? -INFINITY : best;
+            a.status[b] = st;
+            int s = st ? -1 : arg;
+            for (int n = N - 1; n >= 0; --n) {
+                path[n] = s;
+                if (s < 0 || n == 0) continue;
+                s = a.bp16 ? (int)((const short *)a.bp)[bp_base + (size_t)n * K + s]
+                           : ((const int *)a.bp)[bp_base + (size_t)n * K + s];
             }
         }
     }
@@ -818,8 +1014,14 @@ static KFn pick_t(int spt, int T) {
 }
 
 static KFn pick(bool bwd, int mode, int spt, int T) {
-    if (bwd) return mode == MODE_FACTORED ? pick_t<true, MODE_FACTORED>(spt, T) : pick_t<true, MODE_EXACT>(spt, T);
-    return mode == MODE_FACTORED ? pick_t<false, MODE_FACTORED>(spt, T) : pick_t<false, MODE_EXACT>(spt, T);
+    if (bwd) {
+        if (mode == MODE_FACTORED) return pick_t<true, MODE_FACTORED>(spt, T);
+        if (mode == MODE_RAW) return pick_t<true, MODE_RAW>(spt, T);
+        return pick_t<true, MODE_EXACT>(spt, T);
+    }
+    if (mode == MODE_FACTORED) return pick_t<false, MODE_FACTORED>(spt, T);
+    if (mode == MODE_RAW) return pick_t<false, MODE_RAW>(spt, T);
+    return pick_t<false, MODE_EXACT>(spt, T);
 }
 
 static fb_status check_launch(const char *what) {
@@ -828,11 +1030,11 @@ static fb_status check_launch(const char *what) {
     return FB_OK;
 }
 
-static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s) {
+static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw = false) {
     const Graph &G = a.g;
     const bool post_pdf = bwd && a.post_kind != POST_NONE && a.post_kind != POST_STATE;
     size_t sm = smem_bytes(G, bwd, post_pdf) + (post_pdf ? pdf_region(a.post_kind, G.pm.U_max, a.D, a.num_U_max).bytes : 0);
-    KFn fn = pick(bwd, G.mode, G.spt, G.T);
+    KFn fn = pick(bwd, raw ? (int)MODE_RAW : G.mode, G.spt, G.T);
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
     {
@@ -883,7 +1085,7 @@ static WsLayout ws_layout(const Graph &num, const Graph &den, int B, int N_max) 
     WsLayout w;
     size_t o = 0;
     w.den_alpha = o; o += a256((size_t)B * N_max * den.K_tot * 4);
-    w.num_alpha = o; o += a256((size_t)N_max * num.K_tot * 4);
+    w.num_alpha = o; o += a256((size_t)N_max * num.K_tot * 8);  // float64 when the numerator runs raw
     w.gnum = o; o += a256((size_t)N_max * num.pm.U_tot * 4);
     w.zn = o; o += a256((size_t)B * 8);
     w.zd = o; o += a256((size_t)B * 8);
@@ -968,6 +1170,8 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     unsigned char *ws = (unsigned char *)workspace;
     float *den_alpha = (float *)(ws + L.den_alpha);
     float *num_alpha = (float *)(ws + L.num_alpha);
+    double *num_alpha64 = (double *)(ws + L.num_alpha);
+    const bool raw = num->g.mode == MODE_EXACT;  // numerator pass without per-frame normalisation
     float *gnum = (float *)(ws + L.gnum);
     double *zn = (double *)(ws + L.zn), *zd = (double *)(ws + L.zd);
     int *nst = (int *)(ws + L.nst);
@@ -987,11 +1191,13 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     cudaStreamWaitEvent(sr->s, sr->fork, 0);
     {
         FBArgs a = base_args(num, log_emis, lengths, B, N_max);
-        a.lat = num_alpha; a.logZ = zn; a.status = nst;
-        if ((r = launch_fb(false, a, sr->s)) != FB_OK) return r;
+        a.logZ = zn; a.status = nst;
+        if (raw) a.lat64 = num_alpha64; else a.lat = num_alpha;
+        if ((r = launch_fb(false, a, sr->s, raw)) != FB_OK) return r;
         FBArgs c = base_args(num, log_emis, lengths, B, N_max);
-        c.status = nst; c.alpha = num_alpha; c.post = gnum; c.post_kind = POST_PDF_COMPACT;
-        if ((r = launch_fb(true, c, sr->s)) != FB_OK) return r;
+        c.status = nst; c.post = gnum; c.post_kind = POST_PDF_COMPACT;
+        if (raw) { c.alpha64 = num_alpha64; c.logZ_in = zn; } else c.alpha = num_alpha;
+        if ((r = launch_fb(true, c, sr->s, raw)) != FB_OK) return r;
     }
     cudaEventRecord(sr->join, sr->s);
     cudaStreamWaitEvent(s, sr->join, 0);
@@ -1012,16 +1218,53 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
 }
 
 extern "C" size_t fb_viterbi_workspace_bytes(fb_graph g, int32_t B, int32_t N_max) {
-    (void)g; (void)B; (void)N_max;
-    return 0;
+    if (!g || B < 1 || N_max < 1) return 0;
+    const Graph &G = g->g;
+    const size_t per = G.K_max <= 32767 ? 2 : 4;
+    return (size_t)B * G.K_max * (size_t)N_max * per + 256;
 }
 
 extern "C" fb_status fb_viterbi(fb_graph g, const float *log_emis, const int32_t *lengths, int32_t B,
                                 int32_t N_max, double *score, int32_t *path, int32_t *seq_status,
                                 void *workspace, size_t workspace_bytes, void *stream) {
-    (void)g; (void)log_emis; (void)lengths; (void)B; (void)N_max; (void)score; (void)path;
-    (void)seq_status; (void)workspace; (void)workspace_bytes; (void)stream;
-    return FB_ERR_UNSUPPORTED;
+    if (!g || !log_emis || !lengths || !score || !path || !seq_status || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B) || g->g.dry) return FB_ERR_INVALID_ARG;
+    if (!g->g.vit_ok) return FB_ERR_UNSUPPORTED;
+    if (!workspace || workspace_bytes < fb_viterbi_workspace_bytes(g, B, N_max)) return FB_ERR_WORKSPACE;
+    const Graph &G = g->g;
+    VitArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.g = G;
+    a.emis = log_emis;
+    a.lengths = lengths;
+    a.B = B;
+    a.N_max = N_max;
+    a.D = G.D;
+    a.score = score;
+    a.path = path;
+    a.status = seq_status;
+    a.bp = workspace;
+    a.bp16 = G.K_max <= 32767;
+    using VFn = void (*)(VitArgs);
+    VFn fn;
+    const bool small = G.T <= 256;
+    switch (G.spt) {
+        case 1: fn = small ? k_viterbi<1, 256> : k_viterbi<1, 1024>; break;
+        case 2: fn = small ? k_viterbi<2, 256> : k_viterbi<2, 1024>; break;
+        case 3: fn = small ? k_viterbi<3, 256> : k_viterbi<3, 1024>; break;
+        case 4: fn = small ? k_viterbi<4, 256> : k_viterbi<4, 1024>; break;
+        case 6: fn = small ? k_viterbi<6, 256> : k_viterbi<6, 1024>; break;
+        default: fn = small ? k_viterbi<8, 256> : k_viterbi<8, 1024>; break;
+    }
+    const size_t sm = viterbi_smem_bytes(G);
+    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    cudaStream_t s = (cudaStream_t)stream;
+    {
+        ProfScope ps("k_viterbi", s);
+        fn<<<B, G.T, sm, s>>>(a);
+    }
+    return check_launch("k_viterbi launch");
 }
 
 extern "C" void fb_profile_enable(int32_t on) {

@@ -261,3 +261,36 @@ def test_c4_full_size_sampled(fbx):
         assert abs(loss.cpu().numpy()[b] - ref["loss"][0]) <= TOL_LOGZ * max(1, abs(ref["logZ_den"][0]))
         assert np.abs(g[b] - ref["grad"][0]).max() <= TOL_GRAD
     assert np.abs(g.sum(-1)).max() <= 1e-4
+
+
+# ------------------------------------------------------------------ Viterbi (N1)
+
+def _viterbi_check(fbx, graph, emis, lengths):
+    import torch
+
+    g = fbx.Graph.from_host(graph)
+    score, path, st = fbx.fb_viterbi(g, dev(emis), dev(lengths.astype(np.int32)))
+    torch.cuda.synchronize()
+    ref = oracle.viterbi_batch(graph, emis, lengths)
+    st = st.cpu().numpy()
+    assert (st == ref["status"]).all()
+    ok = st == 0
+    # float64 max-plus with the same operand order as the oracle: identical scores and paths
+    assert (score.cpu().numpy()[ok] == ref["score"][ok]).all()
+    assert (path.cpu().numpy() == ref["path"]).all()
+
+
+def test_viterbi_c1(fbx):
+    ws = [synth.make_c1(s) for s in range(100)]
+    _viterbi_check(fbx, synth.compose([w.den for w in ws]), np.concatenate([w.emis for w in ws]),
+                   np.full(100, 6, np.int32))
+
+
+def test_viterbi_c2_numerators(fbx):
+    w = synth.make_c2(seed=2, B=16)
+    _viterbi_check(fbx, synth.compose(w.nums), w.emis, w.lengths)
+
+
+def test_viterbi_c3_den(fbx):
+    w = synth.make_c3(seed=3, B=4, N=80)
+    _viterbi_check(fbx, w.den, w.emis, np.array([80, 13, 1, 55], np.int32))
