@@ -398,7 +398,7 @@ __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, in
 // frame is the one-frame change of the recursion, so exp2 of the vector stays
 // in range (exact fallback otherwise).
 template <bool BWD, int MODE, int SPT, int MAXT>
-__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_fb(const FBArgs a) {
+__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8))) k_fb(const FBArgs a) {
     using V = typename std::conditional<MODE == MODE_FACTORED, float, double>::type;
     constexpr uint32_t VS = sizeof(V);
     constexpr bool RAW = MODE == MODE_RAW;
@@ -1007,9 +1007,10 @@ static KFn pick_spt(int spt) {
     }
 }
 
-// MAXT = 256 variants (≤ 128 registers, two CTAs per SM) for small CTAs; 1024 otherwise.
+// MAXT = 128 variants (six CTAs per SM) and 256 (two per SM) for small CTAs; 1024 otherwise.
 template <bool BWD, int MODE>
 static KFn pick_t(int spt, int T) {
+    if (T <= 128) return pick_spt<BWD, MODE, 128>(spt);
     return T <= 256 ? pick_spt<BWD, MODE, 256>(spt) : pick_spt<BWD, MODE, 1024>(spt);
 }
 
