@@ -390,7 +390,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     if (gr.mode == MODE_FACTORED)
         T = gr.nnz_max >= 16384 ? 1024 : std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 15) / 16)));
     else
-        T = std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 7) / 8)));
+        T = std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 3) / 4)));
     T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
     int spt = (gr.K_max + T - 1) / T;
     spt = spt <= 4 ? spt : (spt <= 6 ? 6 : 8);  // instantiated: 1, 2, 3, 4, 6, 8
@@ -503,7 +503,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.pm.U_tot = slot_off[G];
     if (gr.pm.U_max >= 32768 || (long long)D * 2 > 65536) return FB_ERR_UNSUPPORTED;  // i16 pdf maps in smem
     if (smem_bytes(gr, false, false) > (size_t)kSmemLimit ||
-        smem_bytes(gr, true, true) + pdf_region(POST_GRAD, gr.pm.U_max, D, gr.pm.U_max).bytes > (size_t)kSmemLimit)
+        smem_bytes(gr, true, true) + pdf_region(POST_GRAD, gr.pm.U_max, D).bytes > (size_t)kSmemLimit)
         return FB_ERR_UNSUPPORTED;
 
     // pack and upload

@@ -120,18 +120,14 @@ enum PostKind : int { POST_NONE = 0, POST_STATE = 1, POST_PDF_DENSE = 2, POST_PD
 // Shared-memory region of the pdf-level epilogue, placed after the reductions:
 // ssp   u16[U+1]  slot boundaries of the member's slot-ordered state list
 // pslot i16[D]    pdf → slot (-1 unused)            (dense / grad)
-// nslot i16[D]    pdf → numerator slot (-1 unused)  (grad)
-// gnbuf f32[Un]   one row of numerator pdf posteriors (grad)
 struct PdfRegion {
-    size_t ssp, pslot, nslot, gnbuf, bytes;
+    size_t ssp, pslot, bytes;
 };
-FBX_HD inline PdfRegion pdf_region(int kind, int U_max, int D, int num_U_max) {
+FBX_HD inline PdfRegion pdf_region(int kind, int U_max, int D) {
     PdfRegion R;
     size_t o = 0;
     R.ssp = o; o += fbx_a16((size_t)(U_max + 1) * 2);
     R.pslot = o; if (kind == POST_PDF_DENSE || kind == POST_GRAD) o += fbx_a16((size_t)D * 2);
-    R.nslot = o; if (kind == POST_GRAD) o += fbx_a16((size_t)D * 2);
-    R.gnbuf = o; if (kind == POST_GRAD) o += fbx_a16((size_t)(num_U_max > 0 ? num_U_max : 1) * 4);
     R.bytes = (kind == POST_PDF_DENSE || kind == POST_PDF_COMPACT || kind == POST_GRAD) ? o : 0;
     return R;
 }

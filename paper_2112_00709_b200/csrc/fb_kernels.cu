@@ -337,8 +337,7 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
 // member's slot order, so pdf slot s sums gbuf[ssp[s] .. ssp[s+1]) (ascending
 // state order, ledger L9); maps staged in shared memory (PdfRegion).
 __device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, const unsigned short *ssp,
-                                        const short *pslot, const short *nslot, const float *gnbuf, int gi, int b,
-                                        int n, int tid, int T) {
+                                        const short *pslot, int gi, int b, int n, int tid, int T) {
     const Graph &G = a.g;
     const PdfMap &pm = G.pm;
     if (a.post_kind == POST_PDF_COMPACT) {
@@ -358,12 +357,7 @@ __device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, cons
         float acc = 0.f;
         if (sl >= 0)
             for (int q = ssp[sl]; q < ssp[sl + 1]; ++q) acc += gbuf[q];
-        if (a.post_kind == POST_GRAD) {
-            const int ns = nslot[d];
-            row[d] = (ns >= 0 ? gnbuf[ns] : 0.f) - acc;
-        } else {
-            row[d] = acc;
-        }
+        row[d] = a.post_kind == POST_GRAD ? -acc : acc;  // grad: −Γ_den; Γ_num added by k_add_num
     }
 }
 
@@ -418,11 +412,9 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8
     const uint32_t a_u = sb + (uint32_t)SL.u, a_p = sb + (uint32_t)SL.p, a_part = sb + (uint32_t)SL.part;
     const uint32_t a_wmax = sb + (uint32_t)SL.red, a_wz = a_wmax + 64 * 8, a_flag = a_wmax + 192 * 8;
     float *gbuf = (float *)(smem_raw + SL.gbuf);
-    const PdfRegion PR = pdf_region(a.post_kind, G.pm.U_max, a.D, a.num_U_max);
+    const PdfRegion PR = pdf_region(a.post_kind, G.pm.U_max, a.D);
     unsigned short *ssp = (unsigned short *)(smem_raw + SL.total + PR.ssp);
     short *pslot = (short *)(smem_raw + SL.total + PR.pslot);
-    short *nslot = (short *)(smem_raw + SL.total + PR.nslot);
-    float *gnbuf = (float *)(smem_raw + SL.total + PR.gnbuf);
     const V L2E = (V)1.4426950408889634;
     const V LN2 = (V)0.6931471805599453;
     const V NINF = ninf<V>();
@@ -453,20 +445,12 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8
     }
     if (tid == 0) sts_i(a_flag, 0);
     // pdf-level epilogue maps → shared memory
-    int nU = 0;                    // numerator slots of this utterance (grad)
-    const float *gnrow0 = nullptr; // numerator Γ rows of this utterance (grad)
     if (pdf_post) {
         const int so = G.pm.slot_off[gi], U = G.pm.slot_off[gi + 1] - so;
         const int base = G.pm.slot_sptr[so];
         for (int x = tid; x <= U; x += T) ssp[x] = (unsigned short)(G.pm.slot_sptr[so + x] - base);
         if (a.post_kind != POST_PDF_COMPACT)
             for (int d = tid; d < a.D; d += T) pslot[d] = (short)G.pm.pdf_slot[(size_t)gi * a.D + d];
-        if (a.post_kind == POST_GRAD) {
-            for (int d = tid; d < a.D; d += T) nslot[d] = (short)a.num_pdf_slot[(size_t)b * a.D + d];
-            const int nso = a.num_slot_off[b];
-            nU = a.num_slot_off[b + 1] - nso;
-            gnrow0 = a.gnum + (size_t)a.N_max * nso;
-        }
     }
     const int nsl = S.warp_nsl[gi * W + warp];
     const uint32_t mysl = sb + (uint32_t)SL.rec + (uint32_t)S.warp_off[gi * W + warp];
@@ -511,12 +495,6 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8
     // transitions; backward — the state is reachable from an initial state in n.
     auto viable = [&](int k, int n) { return !use_mask || (BWD ? (distk[k] <= n) : (distk[k] <= N - 1 - n)); };
 
-    // numerator Γ row values (grad epilogue): gq_a for the next posterior row, gq_b the one after
-    auto load_gn = [&](int n) {
-        return (tid < nU) ? __ldg(gnrow0 + (size_t)min(max(n, 0), N - 1) * nU + tid) : 0.f;
-    };
-    float gq_a = 0.f, gq_b = 0.f;
-    if (a.post_kind == POST_GRAD) { gq_a = load_gn(N - 1); gq_b = load_gn(N - 2); }
     float vcur[SPT], vnxt[SPT];  // emissions of the frame being produced and the next one
     V acur[SPT], anxt[SPT];      // α̂ prefetch (backward epilogue), log2 units
     V uk[SPT];                   // this thread's entries of the current vector u (log2)
@@ -590,11 +568,6 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8
                 if (tid + k * T < K) gbuf[posk[k]] = gam;
             }
         }
-        if (a.post_kind == POST_GRAD) {  // numerator Γ row of frame pn (prefetched two frames ago)
-            if (tid < nU) gnbuf[tid] = gq_a;
-            gq_a = gq_b;
-            gq_b = load_gn(pn + 2 * dir);
-        }
     };
     auto block_max_prev = [&](int pp) {
         const V v = lane < W ? lds_v(a_wmax + (uint32_t)(pp * 32 + lane) * 8, (V)0) : NINF;
@@ -650,7 +623,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8
             load_alpha(n_next + dir, anxt);
         }
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
-        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, nslot, gnbuf, gi, b, pend_n, tid, T);
+        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, gi, b, pend_n, tid, T);
         phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
         __syncthreads();
         // ---- phase B of frame n_next
@@ -684,12 +657,12 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8
     // ---- flush the pending posterior rows
     if (want_post) {
         __syncthreads();  // wz[par] of the last frame visible; gbuf of pend_n complete
-        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, nslot, gnbuf, gi, b, pend_n, tid, T);
+        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, gi, b, pend_n, tid, T);
         if (pdf_post) __syncthreads();  // gbuf free again
         posterior(n, par);
         if (pdf_post) {
             __syncthreads();
-            pdf_row(a, gbuf, ssp, pslot, nslot, gnbuf, gi, b, n, tid, T);
+            pdf_row(a, gbuf, ssp, pslot, gi, b, n, tid, T);
         }
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
@@ -956,18 +929,40 @@ __global__ void __launch_bounds__(256) k_posteriors(const Graph G, const float *
     }
 }
 
+// ------------------------------------------------------------------ numerator contribution
+
+// grad[b, n, pdf(s)] += Γ_num[b, n, s] for every numerator slot s (distinct pdfs,
+// so no two threads touch one element: deterministic); sequences flagged by the
+// numerator or the denominator get a zero row.  One CTA per (b, n) row.
+__global__ void __launch_bounds__(256) k_add_num(float *grad, const float *gnum, const int *slot_off,
+                                               const int *slot_pdf, const int *lengths, const int *den_status,
+                                               const int *num_status, int N_max, int D) {
+    const int b = blockIdx.y, n = blockIdx.x;
+    const int N = lengths[b];
+    if (N < 1 || N > N_max || n >= N) return;  // padded rows were zeroed by the den backward
+    float *row = grad + ((size_t)b * N_max + n) * D;
+    if ((den_status[b] | num_status[b]) != 0) {
+        for (int d = threadIdx.x; d < D; d += blockDim.x) row[d] = 0.f;
+        return;
+    }
+    const int so = slot_off[b], U = slot_off[b + 1] - so;
+    const float *g = gnum + (size_t)N_max * so + (size_t)n * U;
+    for (int s = threadIdx.x; s < U; s += blockDim.x) row[slot_pdf[so + s]] += g[s];
+}
+
 // ------------------------------------------------------------------ totals
 
 // loss_b = logZ_num − logZ_den (0 for flagged sequences) and the
 // fixed-order float64 totals {Σ loss, Σ N_b, Σ logZ_num, Σ logZ_den, n_bad}.
-__global__ void k_totals(const double *zn, const double *zd, const int *lengths, const int *status, int B,
-                         double *loss, double *totals) {
+__global__ void k_totals(const double *zn, const double *zd, const int *lengths, int *status, const int *num_status,
+                         int B, double *loss, double *totals) {
     __shared__ double sh[5][256];
     const int tid = threadIdx.x;
     double t[5] = {0, 0, 0, 0, 0};
     // each thread sums a contiguous chunk in ascending b; chunks combine in a fixed tree
     const int chunk = (B + blockDim.x - 1) / blockDim.x;
     for (int b = tid * chunk; b < min(B, (tid + 1) * chunk); ++b) {
+        status[b] |= num_status[b];
         if (status[b] == 0) {
             double l = zn[b] - zd[b];
             loss[b] = l;
@@ -1034,7 +1029,7 @@ static fb_status check_launch(const char *what) {
 static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw = false) {
     const Graph &G = a.g;
     const bool post_pdf = bwd && a.post_kind != POST_NONE && a.post_kind != POST_STATE;
-    size_t sm = smem_bytes(G, bwd, post_pdf) + (post_pdf ? pdf_region(a.post_kind, G.pm.U_max, a.D, a.num_U_max).bytes : 0);
+    size_t sm = smem_bytes(G, bwd, post_pdf) + (post_pdf ? pdf_region(a.post_kind, G.pm.U_max, a.D).bytes : 0);
     KFn fn = pick(bwd, raw ? (int)MODE_RAW : G.mode, G.spt, G.T);
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
@@ -1201,19 +1196,24 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
         if ((r = launch_fb(true, c, sr->s, raw)) != FB_OK) return r;
     }
     cudaEventRecord(sr->join, sr->s);
-    cudaStreamWaitEvent(s, sr->join, 0);
-    // denominator backward + fused posterior/gradient epilogue + loss
+    // denominator backward + fused −Γ_den gradient epilogue: independent of the numerator
     {
         FBArgs c = base_args(den, log_emis, lengths, B, N_max);
-        c.status = seq_status; c.status2 = nst; c.alpha = den_alpha;
+        c.status = seq_status; c.alpha = den_alpha;
         c.post = grad; c.post_kind = POST_GRAD;
-        c.gnum = gnum; c.num_slot_off = num->g.pm.slot_off; c.num_pdf_slot = num->g.pm.pdf_slot;
-        c.num_U_max = num->g.pm.U_max;
         if ((r = launch_fb(true, c, s)) != FB_OK) return r;
     }
+    cudaStreamWaitEvent(s, sr->join, 0);
+    {
+        ProfScope ps("k_add_num", s);
+        k_add_num<<<dim3((unsigned)N_max, (unsigned)B), 256, 0, s>>>(grad, gnum, num->g.pm.slot_off,
+                                                                    num->g.pm.slot_pdf, lengths, seq_status, nst,
+                                                                    N_max, num->g.D);
+    }
+    if ((r = check_launch("k_add_num launch")) != FB_OK) return r;
     {
         ProfScope ps("k_totals", s);
-        k_totals<<<1, 256, 0, s>>>(zn, zd, lengths, seq_status, B, loss, totals);
+        k_totals<<<1, 256, 0, s>>>(zn, zd, lengths, seq_status, nst, B, loss, totals);
     }
     return check_launch("k_totals launch");
 }
