@@ -391,14 +391,13 @@ __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, in
 // float64 offset accumulates c_n exactly, and the largest entry of each stored
 // frame is the one-frame change of the recursion, so exp2 of the vector stays
 // in range (exact fallback otherwise).
-template <bool BWD, int MODE, int SPT, int MAXT>
-__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8))) k_fb(const FBArgs a) {
+template <bool BWD, int MODE, int SPT>
+__device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     using V = typename std::conditional<MODE == MODE_FACTORED, float, double>::type;
     constexpr uint32_t VS = sizeof(V);
     constexpr bool RAW = MODE == MODE_RAW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Graph &G = a.g;
-    const int b = blockIdx.x;
     const int gi = (G.G == 1) ? 0 : b;
     const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
     const int s0 = G.state_off[gi];
@@ -702,6 +701,17 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8
                 a.status[b] = stt;
             }
         }
+    }
+}
+
+// Sequences b = blockIdx.x, blockIdx.x + gridDim.x, …  (gridDim.x = B normally;
+// fewer, persistent CTAs confine the numerator pass of lfmmi_loss_grad to the
+// SMs the denominator leaves idle).
+template <bool BWD, int MODE, int SPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8))) k_fb(const FBArgs a) {
+    for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+        fb_sequence<BWD, MODE, SPT>(a, b);
+        __syncthreads();  // shared memory is reused by the next sequence
     }
 }
 
@@ -1026,7 +1036,8 @@ static fb_status check_launch(const char *what) {
     return FB_OK;
 }
 
-static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw = false) {
+// idle_sms > 0: launch only as many (persistent) CTAs as fit on that many SMs.
+static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw = false, int idle_sms = 0) {
     const Graph &G = a.g;
     const bool post_pdf = bwd && a.post_kind != POST_NONE && a.post_kind != POST_STATE;
     size_t sm = smem_bytes(G, bwd, post_pdf) + (post_pdf ? pdf_region(a.post_kind, G.pm.U_max, a.D).bytes : 0);
@@ -1035,7 +1046,13 @@ static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw =
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
     {
         ProfScope ps(bwd ? (G.G == 1 ? "k_fb_bwd[G=1]" : "k_fb_bwd[G=B]") : (G.G == 1 ? "k_fb_fwd[G=1]" : "k_fb_fwd[G=B]"), s);
-        fn<<<a.B, G.T, sm, s>>>(a);
+        int grid = a.B;
+        if (idle_sms > 0) {
+            int occ = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G.T, sm);
+            grid = std::max(1, std::min(a.B, idle_sms * std::max(occ, 1)));
+        }
+        fn<<<grid, G.T, sm, s>>>(a);
     }
     return check_launch("k_fb launch");
 }
@@ -1185,15 +1202,21 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
         if ((r = launch_fb(false, a, s)) != FB_OK) return r;
     }
     cudaStreamWaitEvent(sr->s, sr->fork, 0);
+    // SMs the denominator passes leave idle (one den CTA per SM)
+    int dev = 0, nsm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int idle = nsm - std::min(B, nsm);
+    const int confine = idle >= 8 ? idle : 0;
     {
         FBArgs a = base_args(num, log_emis, lengths, B, N_max);
         a.logZ = zn; a.status = nst;
         if (raw) a.lat64 = num_alpha64; else a.lat = num_alpha;
-        if ((r = launch_fb(false, a, sr->s, raw)) != FB_OK) return r;
+        if ((r = launch_fb(false, a, sr->s, raw, confine)) != FB_OK) return r;
         FBArgs c = base_args(num, log_emis, lengths, B, N_max);
         c.status = nst; c.post = gnum; c.post_kind = POST_PDF_COMPACT;
         if (raw) { c.alpha64 = num_alpha64; c.logZ_in = zn; } else c.alpha = num_alpha;
-        if ((r = launch_fb(true, c, sr->s, raw)) != FB_OK) return r;
+        if ((r = launch_fb(true, c, sr->s, raw, confine)) != FB_OK) return r;
     }
     cudaEventRecord(sr->join, sr->s);
     // denominator backward + fused −Γ_den gradient epilogue: independent of the numerator
