@@ -494,22 +494,25 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     // transitions; backward — the state is reachable from an initial state in n.
     auto viable = [&](int k, int n) { return !use_mask || (BWD ? (distk[k] <= n) : (distk[k] <= N - 1 - n)); };
 
-    float vcur[SPT], vnxt[SPT];  // emissions of the frame being produced and the next one
-    V acur[SPT], anxt[SPT];      // α̂ prefetch (backward epilogue), log2 units
-    V uk[SPT];                   // this thread's entries of the current vector u (log2)
-    V xpost[SPT];                // α̂_n + β̂_n of the frame whose posterior is pending
+    // Ping-pong prefetch buffers (A: even steps, B: odd steps): a buffer is
+    // consumed by its frame's phase B and immediately refilled with the frame
+    // two steps ahead, so loads have a whole frame of slack and no register moves.
+    float vA[SPT], vB[SPT];  // emissions
+    V aA[SPT], aB[SPT];      // α̂ (backward epilogue), log2 units
+    V uk[SPT];               // this thread's entries of the current vector u (log2)
+    V xpost[SPT];            // α̂_n + β̂_n of the frame whose posterior is pending
     const int dir = BWD ? -1 : 1;
     const int n_first = BWD ? N - 1 : 0;
-    load_v(n_first, vcur);
-    load_v(n_first + dir, vnxt);
-    if (want_post) { load_alpha(n_first, acur); load_alpha(n_first + dir, anxt); }
+    load_v(n_first, vA);
+    load_v(n_first + dir, vB);
+    if (want_post) { load_alpha(n_first, aA); load_alpha(n_first + dir, aB); }
     double scale = 0.0;  // C_n (fwd) / D_n (bwd), log2 units
     float vsum = 0.f;    // Σ of every emission read: NaN / +∞ ⇒ non-finite input
     int par = 0;         // parity of the reduction buffers of the current frame
 
     // Store frame n's normalised values h (α̂_n or β̂_n) and u; reduce max(u) and,
     // in the backward, the log-sum-exp of x = α̂_n + β̂_n into buffers [par].
-    auto emit = [&](int n, const V *h) {
+    auto emit = [&](int n, const V *h, const V *acur) {
         float *latn = (!RAW && a.lat) ? a.lat + lat_base + (size_t)n * K : nullptr;
         double *latn64 = (RAW && a.lat64) ? a.lat64 + lat_base + (size_t)n * K : nullptr;
         V lmax = NINF;
@@ -581,7 +584,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         for (int k = 0; k < SPT; ++k) {
             const int j = tid + k * T;
             const bool ok = j < K && viable(k, n_first);
-            const float v = vcur[k];
+            const float v = vA[k];
             vsum += v;
             const V v2 = (V)v * L2E;
             if (!BWD) {
@@ -604,23 +607,16 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k) { h[k] -= c; uk[k] -= c; }
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n_first] = scale * kLN2;
-        emit(n_first, h);
+        emit(n_first, h, aA);
+        load_v(n_first + 2 * dir, vA);
+        if (want_post) load_alpha(n_first + 2 * dir, aA);
     }
     int n = n_first;
     int pend_n = n_first;  // frame whose posterior is pending
-    for (;;) {
+    auto step = [&](float (&vb)[SPT], V (&ab)[SPT]) -> bool {
         const int n_next = n + dir;
-        if (BWD ? (n_next < 0) : (n_next >= N)) break;
+        if (BWD ? (n_next < 0) : (n_next >= N)) return false;
         __syncthreads();  // u, p, wmax[par], wz[par] of frame n visible
-        // rotate prefetch: frame n_next becomes current, issue n_next + dir
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) vcur[k] = vnxt[k];
-        load_v(n_next + dir, vnxt);
-        if (want_post) {
-#pragma unroll
-            for (int k = 0; k < SPT; ++k) acur[k] = anxt[k];
-            load_alpha(n_next + dir, anxt);
-        }
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
         if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, gi, b, pend_n, tid, T);
         phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
@@ -640,7 +636,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         for (int k = 0; k < SPT; ++k) {
             const V y = lds_v(a_part + (uint32_t)(tid + k * T) * VS, (V)0);
             const bool ok = viable(k, n);
-            const float v = vcur[k];
+            const float v = vb[k];
             vsum += v;
             const V v2 = (V)v * L2E;
             if (!BWD) {
@@ -651,7 +647,14 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
                 uk[k] = h[k] + v2;
             }
         }
-        emit(n, h);
+        emit(n, h, ab);
+        load_v(n + 2 * dir, vb);  // refill with the frame two steps ahead
+        if (want_post) load_alpha(n + 2 * dir, ab);
+        return true;
+    };
+    for (;;) {
+        if (!step(vB, aB)) break;
+        if (!step(vA, aA)) break;
     }
     // ---- flush the pending posterior rows
     if (want_post) {
