@@ -352,12 +352,16 @@ __device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, cons
     }
     const int D = a.D;
     float *row = a.post + ((size_t)b * a.N_max + n) * D;
+    const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;  // grad: −Γ_den; Γ_num added by k_add_num
     for (int d = tid; d < D; d += T) {
         const int sl = pslot[d];
         float acc = 0.f;
-        if (sl >= 0)
-            for (int q = ssp[sl]; q < ssp[sl + 1]; ++q) acc += gbuf[q];
-        row[d] = a.post_kind == POST_GRAD ? -acc : acc;  // grad: −Γ_den; Γ_num added by k_add_num
+        if (sl >= 0) {
+            const int q0 = ssp[sl], q1 = ssp[sl + 1];
+            acc = gbuf[q0];
+            for (int q = q0 + 1; q < q1; ++q) acc += gbuf[q];
+        }
+        row[d] = sgn * acc;
     }
 }
 
