@@ -715,7 +715,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 // fewer, persistent CTAs confine the numerator pass of lfmmi_loss_grad to the
 // SMs the denominator leaves idle).
 template <bool BWD, int MODE, int SPT, int MAXT>
-__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 8))) k_fb(const FBArgs a) {
+__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 7))) k_fb(const FBArgs a) {
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         fb_sequence<BWD, MODE, SPT>(a, b);
         __syncthreads();  // shared memory is reused by the next sequence
