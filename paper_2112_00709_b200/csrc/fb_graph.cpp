@@ -390,7 +390,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     if (gr.mode == MODE_FACTORED)
         T = gr.nnz_max >= 16384 ? 1024 : std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 15) / 16)));
     else
-        T = std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 3) / 4)));
+        T = std::min(1024, std::max(128, pow2ceil((gr.nnz_max + 7) / 8)));
     if (const char *e = std::getenv("FBX_EXACT_T"); e && gr.mode == MODE_EXACT) T = std::max(32, std::atoi(e));
     T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
     int spt = (gr.K_max + T - 1) / T;

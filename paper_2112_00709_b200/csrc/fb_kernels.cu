@@ -335,17 +335,24 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
 
 // Write one frame's pdf-level posterior (or gradient) row.  gbuf holds γ in the
 // member's slot order, so pdf slot s sums gbuf[ssp[s] .. ssp[s+1]) (ascending
-// state order, ledger L9); maps staged in shared memory (PdfRegion).
-__device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, const unsigned short *ssp,
-                                        const short *pslot, int gi, int b, int n, int tid, int T) {
+// state order, ledger L9); maps staged in shared memory (PdfRegion), addressed
+// through the 32-bit shared window.
+__device__ __forceinline__ int lds_s16(uint32_t a) {
+    short v;
+    asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(a));
+    return (int)v;
+}
+__device__ __forceinline__ void pdf_row(const FBArgs &a, uint32_t a_gbuf, uint32_t a_ssp, uint32_t a_pslot, int gi,
+                                        int b, int n, int tid, int T) {
     const Graph &G = a.g;
     const PdfMap &pm = G.pm;
     if (a.post_kind == POST_PDF_COMPACT) {
         const int so = pm.slot_off[gi], U = pm.slot_off[gi + 1] - so;
         float *row = a.post + (size_t)a.N_max * so + (size_t)n * U;
         for (int sl = tid; sl < U; sl += T) {
+            const int q0 = (int)lds_u16(a_ssp + 2 * sl), q1 = (int)lds_u16(a_ssp + 2 * sl + 2);
             float acc = 0.f;
-            for (int q = ssp[sl]; q < ssp[sl + 1]; ++q) acc += gbuf[q];
+            for (int q = q0; q < q1; ++q) acc += lds_v(a_gbuf + 4 * q, 0.f);
             row[sl] = acc;
         }
         return;
@@ -354,12 +361,12 @@ __device__ __forceinline__ void pdf_row(const FBArgs &a, const float *gbuf, cons
     float *row = a.post + ((size_t)b * a.N_max + n) * D;
     const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;  // grad: −Γ_den; Γ_num added by k_add_num
     for (int d = tid; d < D; d += T) {
-        const int sl = pslot[d];
+        const int sl = lds_s16(a_pslot + 2 * d);
         float acc = 0.f;
         if (sl >= 0) {
-            const int q0 = ssp[sl], q1 = ssp[sl + 1];
-            acc = gbuf[q0];
-            for (int q = q0 + 1; q < q1; ++q) acc += gbuf[q];
+            const int q0 = (int)lds_u16(a_ssp + 2 * sl), q1 = (int)lds_u16(a_ssp + 2 * sl + 2);
+            acc = lds_v(a_gbuf + 4 * q0, 0.f);
+            for (int q = q0 + 1; q < q1; ++q) acc += lds_v(a_gbuf + 4 * q, 0.f);
         }
         row[d] = sgn * acc;
     }
@@ -418,6 +425,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     const PdfRegion PR = pdf_region(a.post_kind, G.pm.U_max, a.D);
     unsigned short *ssp = (unsigned short *)(smem_raw + SL.total + PR.ssp);
     short *pslot = (short *)(smem_raw + SL.total + PR.pslot);
+    const uint32_t a_gbuf = sb + (uint32_t)SL.gbuf;
+    const uint32_t a_ssp = sb + (uint32_t)(SL.total + PR.ssp), a_pslot = sb + (uint32_t)(SL.total + PR.pslot);
     const V L2E = (V)1.4426950408889634;
     const V LN2 = (V)0.6931471805599453;
     const V NINF = ninf<V>();
@@ -484,14 +493,15 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k) v[k] = __ldg(row + pdfk[k]);
     };
-    // α̂ of frame n in log2 units (float natural-log lattice, or the raw float64 log2 one)
+    // α̂ of frame n as stored (float natural log, or the raw float64 log2 lattice);
+    // converted to log2 at use so the load is not waited on at issue
     auto load_alpha = [&](int n, V *v) {
         const size_t ro = lat_base + (size_t)min(max(n, 0), N - 1) * K;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int j = min(tid + k * T, K - 1);
             if (RAW) v[k] = (V)__ldg(a.alpha64 + ro + j);
-            else v[k] = (V)__ldg(a.alpha + ro + j) * L2E;
+            else v[k] = (V)__ldg(a.alpha + ro + j);
         }
     };
     // viable(k, n): forward — a final state is reachable in the N-1-n remaining
@@ -535,7 +545,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         }
         if (want_post) {
 #pragma unroll
-            for (int k = 0; k < SPT; ++k) xpost[k] = (tid + k * T < K) ? acur[k] + h[k] : NINF;
+            for (int k = 0; k < SPT; ++k)
+                xpost[k] = (tid + k * T < K) ? (RAW ? acur[k] : acur[k] * L2E) + h[k] : NINF;
         }
         if (want_post && !RAW) {
             V zm;
@@ -571,7 +582,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
                 const float gam = (Z == NINF) ? 0.f : ex2((float)(xpost[k] - Zs));
-                if (tid + k * T < K) gbuf[posk[k]] = gam;
+                if (tid + k * T < K) sts_v(a_gbuf + 4 * (uint32_t)posk[k], gam);
             }
         }
     };
@@ -622,7 +633,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         if (BWD ? (n_next < 0) : (n_next >= N)) return false;
         __syncthreads();  // u, p, wmax[par], wz[par] of frame n visible
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
-        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, gi, b, pend_n, tid, T);
+        if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pslot, gi, b, pend_n, tid, T);
         phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
         __syncthreads();
         // ---- phase B of frame n_next
@@ -663,12 +674,12 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     // ---- flush the pending posterior rows
     if (want_post) {
         __syncthreads();  // wz[par] of the last frame visible; gbuf of pend_n complete
-        if (pdf_post && pend_n != n) pdf_row(a, gbuf, ssp, pslot, gi, b, pend_n, tid, T);
+        if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pslot, gi, b, pend_n, tid, T);
         if (pdf_post) __syncthreads();  // gbuf free again
         posterior(n, par);
         if (pdf_post) {
             __syncthreads();
-            pdf_row(a, gbuf, ssp, pslot, gi, b, n, tid, T);
+            pdf_row(a, a_gbuf, a_ssp, a_pslot, gi, b, n, tid, T);
         }
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
