@@ -29,6 +29,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -213,6 +215,27 @@ __device__ __forceinline__ void sts_v(uint32_t a, double v) { asm volatile("st.s
 __device__ __forceinline__ void sts_i(uint32_t a, int v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
 __device__ __forceinline__ int lds_i(uint32_t a) { return (int)lds_u32(a); }
 
+// TMA bulk copy global → shared with mbarrier completion (Hopper+/Blackwell).
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAIT_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
 // Block log-sum-exp from per-warp (m, s) pairs in (generic) shared memory.
 template <class V>
 __device__ __forceinline__ V block_lse_from(const double *wz, int W, int lane) {
@@ -242,6 +265,7 @@ struct FBArgs {
     const int *num_slot_off;
     const int *num_pdf_slot; // [B*D]
     int num_U_max;           // largest numerator slot count (gnbuf size)
+    int tma;                 // stage φ rows in shared memory with TMA bulk copies
     // MODE_RAW (lfmmi numerator): float64 log2 lattices, posteriors normalised by logZ_in
     double *lat64;
     const double *alpha64;
@@ -426,6 +450,11 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     unsigned short *ssp = (unsigned short *)(smem_raw + SL.total + PR.ssp);
     short *pslot = (short *)(smem_raw + SL.total + PR.pslot);
     const uint32_t a_gbuf = sb + (uint32_t)SL.gbuf;
+    // φ row staging (TMA): two row buffers + two mbarriers after the pdf region
+    const bool use_tma = a.tma != 0;
+    const uint32_t rowbytes = (uint32_t)a.D * 4;
+    const uint32_t a_ebuf = sb + (uint32_t)(SL.total + PR.bytes);
+    const uint32_t a_mbar = a_ebuf + (uint32_t)fbx_a16(2 * (size_t)rowbytes);
     const uint32_t a_ssp = sb + (uint32_t)(SL.total + PR.ssp), a_pslot = sb + (uint32_t)(SL.total + PR.pslot);
     const V L2E = (V)1.4426950408889634;
     const V LN2 = (V)0.6931471805599453;
@@ -489,10 +518,39 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     const float *em = a.emis + (size_t)b * a.N_max * a.D;
     const size_t lat_base = (size_t)a.N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
     auto load_v = [&](int n, float *v) {
+        if (use_tma) return;  // rows arrive in shared memory instead
         const float *row = em + (size_t)min(max(n, 0), N - 1) * a.D;
 #pragma unroll
         for (int k = 0; k < SPT; ++k) v[k] = __ldg(row + pdfk[k]);
     };
+    // TMA: step t (t-th frame processed) uses buffer t & 1, whose (t >> 1)-th
+    // completion has parity (t >> 1) & 1.  Issued by one thread one step ahead.
+    auto tma_issue = [&](int t, int n) {
+        if (!use_tma || tid != 0) return;
+        if (n < 0 || n >= N) return;
+        const uint32_t mb = a_mbar + 8u * (uint32_t)(t & 1);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(mb, rowbytes);
+        tma_g2s(a_ebuf + (uint32_t)(t & 1) * rowbytes, em + (size_t)n * a.D, rowbytes, mb);
+    };
+    // this thread's emissions of the frame processed at step t
+    auto fetch_v = [&](int t, const float *vreg, float *v) {
+        if (!use_tma) {
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) v[k] = vreg[k];
+            return;
+        }
+        mbar_wait(a_mbar + 8u * (uint32_t)(t & 1), (uint32_t)((t >> 1) & 1));
+        const uint32_t base = a_ebuf + (uint32_t)(t & 1) * rowbytes;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) v[k] = lds_v(base + 4u * (uint32_t)pdfk[k], 0.f);
+    };
+    if (use_tma && tid == 0) {
+        mbar_init(a_mbar, 1);
+        mbar_init(a_mbar + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (use_tma) __syncthreads();  // barriers initialised before anyone waits on them
     // α̂ of frame n as stored (float natural log, or the raw float64 log2 lattice);
     // converted to log2 at use so the load is not waited on at issue
     auto load_alpha = [&](int n, V *v) {
@@ -519,6 +577,9 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     const int n_first = BWD ? N - 1 : 0;
     load_v(n_first, vA);
     load_v(n_first + dir, vB);
+    tma_issue(0, n_first);
+    tma_issue(1, n_first + dir);
+    int tstep = 0;  // index of the frame being produced (t in tma_issue / fetch_v)
     if (want_post) { load_alpha(n_first, aA); load_alpha(n_first + dir, aB); }
     double scale = 0.0;  // C_n (fwd) / D_n (bwd), log2 units
     float vsum = 0.f;    // Σ of every emission read: NaN / +∞ ⇒ non-finite input
@@ -595,11 +656,13 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     {
         V h[SPT];
         V lmax = NINF;
+        float vv[SPT];
+        fetch_v(0, vA, vv);
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int j = tid + k * T;
             const bool ok = j < K && viable(k, n_first);
-            const float v = vA[k];
+            const float v = vv[k];
             vsum += v;
             const V v2 = (V)v * L2E;
             if (!BWD) {
@@ -632,6 +695,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         const int n_next = n + dir;
         if (BWD ? (n_next < 0) : (n_next >= N)) return false;
         __syncthreads();  // u, p, wmax[par], wz[par] of frame n visible
+        ++tstep;
+        tma_issue(tstep + 1, n_next + dir);  // buffer of step tstep-1 is free now
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
         if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pslot, gi, b, pend_n, tid, T);
         phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
@@ -647,11 +712,13 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         scale += (double)c;
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
         V h[SPT];
+        float vv[SPT];
+        fetch_v(tstep, vb, vv);
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const V y = lds_v(a_part + (uint32_t)(tid + k * T) * VS, (V)0);
             const bool ok = viable(k, n);
-            const float v = vb[k];
+            const float v = vv[k];
             vsum += v;
             const V v2 = (V)v * L2E;
             if (!BWD) {
@@ -719,6 +786,10 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
                 a.status[b] = stt;
             }
         }
+    }
+    if (use_tma && tid == 0) {  // all TMA rows were consumed; the next sequence re-initialises
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(a_mbar) : "memory");
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(a_mbar + 8) : "memory");
     }
 }
 
@@ -1059,6 +1130,12 @@ static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw =
     const Graph &G = a.g;
     const bool post_pdf = bwd && a.post_kind != POST_NONE && a.post_kind != POST_STATE;
     size_t sm = smem_bytes(G, bwd, post_pdf) + (post_pdf ? pdf_region(a.post_kind, G.pm.U_max, a.D).bytes : 0);
+    // φ rows through TMA when they are 16-byte aligned and the two row buffers fit
+    const size_t tma_bytes = fbx_a16(2 * (size_t)a.D * 4) + 16;
+    FBArgs aa = a;
+    aa.tma = (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0) && sm + tma_bytes <= (size_t)kSmemLimit &&
+             std::getenv("FBX_NO_TMA") == nullptr;
+    if (aa.tma) sm += tma_bytes;
     KFn fn = pick(bwd, raw ? (int)MODE_RAW : G.mode, G.spt, G.T);
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
@@ -1070,7 +1147,7 @@ static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw =
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G.T, sm);
             grid = std::max(1, std::min(a.B, idle_sms * std::max(occ, 1)));
         }
-        fn<<<grid, G.T, sm, s>>>(a);
+        fn<<<grid, G.T, sm, s>>>(aa);
     }
     return check_launch("k_fb launch");
 }
