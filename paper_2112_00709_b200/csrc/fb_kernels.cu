@@ -426,8 +426,13 @@ __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, in
 // float64 offset accumulates c_n exactly, and the largest entry of each stored
 // frame is the one-frame change of the recursion, so exp2 of the vector stays
 // in range (exact fallback otherwise).
-template <bool BWD, int MODE, int SPT>
+// MODEX: MODE_FACTORED / MODE_EXACT / MODE_RAW, or kModeFactoredTma (factored
+// arithmetic with φ rows staged through TMA).
+constexpr int kModeFactoredTma = 4;
+template <bool BWD, int MODEX, int SPT>
 __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
+    constexpr bool TMA = MODEX == kModeFactoredTma;
+    constexpr int MODE = TMA ? (int)MODE_FACTORED : MODEX;
     using V = typename std::conditional<MODE == MODE_FACTORED, float, double>::type;
     constexpr uint32_t VS = sizeof(V);
     constexpr bool RAW = MODE == MODE_RAW;
@@ -451,7 +456,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     short *pslot = (short *)(smem_raw + SL.total + PR.pslot);
     const uint32_t a_gbuf = sb + (uint32_t)SL.gbuf;
     // φ row staging (TMA): two row buffers + two mbarriers after the pdf region
-    const bool use_tma = a.tma != 0;
+    constexpr bool use_tma = TMA;
     const uint32_t rowbytes = (uint32_t)a.D * 4;
     const uint32_t a_ebuf = sb + (uint32_t)(SL.total + PR.bytes);
     const uint32_t a_mbar = a_ebuf + (uint32_t)fbx_a16(2 * (size_t)rowbytes);
@@ -796,10 +801,10 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 // Sequences b = blockIdx.x, blockIdx.x + gridDim.x, …  (gridDim.x = B normally;
 // fewer, persistent CTAs confine the numerator pass of lfmmi_loss_grad to the
 // SMs the denominator leaves idle).
-template <bool BWD, int MODE, int SPT, int MAXT>
+template <bool BWD, int MODEX, int SPT, int MAXT>
 __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 7))) k_fb(const FBArgs a) {
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-        fb_sequence<BWD, MODE, SPT>(a, b);
+        fb_sequence<BWD, MODEX, SPT>(a, b);
         __syncthreads();  // shared memory is reused by the next sequence
     }
 }
@@ -1110,10 +1115,12 @@ static KFn pick_t(int spt, int T) {
 
 static KFn pick(bool bwd, int mode, int spt, int T) {
     if (bwd) {
+        if (mode == kModeFactoredTma) return pick_t<true, kModeFactoredTma>(spt, T);
         if (mode == MODE_FACTORED) return pick_t<true, MODE_FACTORED>(spt, T);
         if (mode == MODE_RAW) return pick_t<true, MODE_RAW>(spt, T);
         return pick_t<true, MODE_EXACT>(spt, T);
     }
+    if (mode == kModeFactoredTma) return pick_t<false, kModeFactoredTma>(spt, T);
     if (mode == MODE_FACTORED) return pick_t<false, MODE_FACTORED>(spt, T);
     if (mode == MODE_RAW) return pick_t<false, MODE_RAW>(spt, T);
     return pick_t<false, MODE_EXACT>(spt, T);
@@ -1133,10 +1140,10 @@ static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw =
     // φ rows through TMA when they are 16-byte aligned and the two row buffers fit
     const size_t tma_bytes = fbx_a16(2 * (size_t)a.D * 4) + 16;
     FBArgs aa = a;
-    aa.tma = (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0) && sm + tma_bytes <= (size_t)kSmemLimit &&
-             std::getenv("FBX_NO_TMA") == nullptr;
+    aa.tma = G.mode == MODE_FACTORED && !raw && (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0) &&
+             sm + tma_bytes <= (size_t)kSmemLimit && std::getenv("FBX_NO_TMA") == nullptr;
     if (aa.tma) sm += tma_bytes;
-    KFn fn = pick(bwd, raw ? (int)MODE_RAW : G.mode, G.spt, G.T);
+    KFn fn = pick(bwd, raw ? (int)MODE_RAW : (aa.tma ? kModeFactoredTma : G.mode), G.spt, G.T);
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
     {
