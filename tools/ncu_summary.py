@@ -59,7 +59,10 @@ for k, lst in agg.items():
           f"conf={avg.get('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 0)/1e6:.0f}M "
           f"xu={avg.get('sm__inst_executed_pipe_xu.sum', 0)/1e6:.0f}M regs={avg.get('launch__registers_per_thread', 0):.0f}")
 if out_json:
-    names = {"k_fb<1, 0, 3, 1024>": "k_fb_bwd[G=1]", "k_fb<0, 0, 3, 1024>": "k_fb_fwd[G=1]"}
+    names = {}
+    for k in summary:
+        if k.startswith("k_fb<") and k.endswith(", 1024>") and k.split(",")[1].strip() in ("0", "4"):
+            names[k] = "k_fb_bwd[G=1]" if k.startswith("k_fb<1") else "k_fb_fwd[G=1]"
     traffic = {}
     for k, avg in summary.items():
         key = names.get(k, k)
