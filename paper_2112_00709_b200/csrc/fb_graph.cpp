@@ -392,6 +392,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     else
         T = std::min(1024, std::max(128, pow2ceil((gr.nnz_max + 7) / 8)));
     if (const char *e = std::getenv("FBX_EXACT_T"); e && gr.mode == MODE_EXACT) T = std::max(32, std::atoi(e));
+    if (const char *e = std::getenv("FBX_FACT_T"); e && gr.mode == MODE_FACTORED) T = std::max(32, std::atoi(e));
     T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
     int spt = (gr.K_max + T - 1) / T;
     spt = spt <= 4 ? spt : (spt <= 6 ? 6 : 8);  // instantiated: 1, 2, 3, 4, 6, 8

@@ -802,7 +802,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 // fewer, persistent CTAs confine the numerator pass of lfmmi_loss_grad to the
 // SMs the denominator leaves idle).
 template <bool BWD, int MODEX, int SPT, int MAXT>
-__global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : (MAXT == 256 ? 2 : 7))) k_fb(const FBArgs a) {
+__global__ void __launch_bounds__(MAXT, (MAXT >= 512 ? 1 : (MAXT == 256 ? 2 : 7))) k_fb(const FBArgs a) {
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         fb_sequence<BWD, MODEX, SPT>(a, b);
         __syncthreads();  // shared memory is reused by the next sequence
@@ -1110,7 +1110,10 @@ static KFn pick_spt(int spt) {
 template <bool BWD, int MODE>
 static KFn pick_t(int spt, int T) {
     if (T <= 128) return pick_spt<BWD, MODE, 128>(spt);
-    return T <= 256 ? pick_spt<BWD, MODE, 256>(spt) : pick_spt<BWD, MODE, 1024>(spt);
+    if (T <= 256) return pick_spt<BWD, MODE, 256>(spt);
+    if constexpr (MODE == MODE_FACTORED || MODE == kModeFactoredTma)
+        if (T <= 512) return pick_spt<BWD, MODE, 512>(spt);  // ≤ 128 registers per thread
+    return pick_spt<BWD, MODE, 1024>(spt);
 }
 
 static KFn pick(bool bwd, int mode, int spt, int T) {
