@@ -85,8 +85,7 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     }
     const long long nnz_m = rl.ptr[K];
     const long long P = std::max<long long>(1, (nnz_m + 32LL * W - 1) / (32LL * W));  // slots per warp
-    int target = (int)std::max<long long>(4, P / 2);
-    if (const char *e = std::getenv("FBX_SLICE_TARGET")) target = std::max(1, std::atoi(e));
+    const int target = (int)std::max<long long>(4, P / 2);
     struct Slice { int lg, L; std::vector<Block> blk; };
     std::vector<Slice> sl;
     for (size_t i = 0; i < blocks.size();) {
