@@ -65,43 +65,25 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
         while (lg < 5 && (d + (1LL << lg) - 1) / (1LL << lg) > Lmax) ++lg;
         cls[lg].push_back({r, (int)((d + (1LL << lg) - 1) / (1LL << lg))});
     }
-    // blocks: 32/g rows of one g class with equal padded length L (one row
-    // segment per lane); slices: up to R consecutive blocks of equal (lg, L), so
-    // the per-slice decode is amortised over R rows per lane
-    struct Block { int lg, L; std::vector<int> rows; };
-    std::vector<Block> blocks;
+    struct Slice { int lg, L; std::vector<int> rows; };
+    std::vector<Slice> sl;
     for (int lg = 0; lg < 6; ++lg) {
         auto &c = cls[lg];
         std::stable_sort(c.begin(), c.end(), [](const RowG &a, const RowG &b) { return a.len > b.len; });
         const int per = 32 >> lg;
         for (size_t i = 0; i < c.size(); i += per) {
-            Block bk;
-            bk.lg = lg;
-            bk.L = (c[i].len + 1) & ~1;
-            if (bk.L / 2 >= (1 << 13)) return false;
-            for (size_t t = i; t < std::min(c.size(), i + per); ++t) bk.rows.push_back(c[t].row);
-            blocks.push_back(std::move(bk));
+            Slice s;
+            s.lg = lg;
+            s.L = (c[i].len + 1) & ~1;
+            if (s.L / 2 >= (1 << 13)) return false;
+            for (size_t t = i; t < std::min(c.size(), i + per); ++t) s.rows.push_back(c[t].row);
+            sl.push_back(std::move(s));
         }
-    }
-    const long long nnz_m = rl.ptr[K];
-    const long long P = std::max<long long>(1, (nnz_m + 32LL * W - 1) / (32LL * W));  // slots per warp
-    const int target = (int)std::max<long long>(4, P / 2);
-    struct Slice { int lg, L; std::vector<Block> blk; };
-    std::vector<Slice> sl;
-    for (size_t i = 0; i < blocks.size();) {
-        Slice s;
-        s.lg = blocks[i].lg;
-        s.L = blocks[i].L;
-        const int rmax = std::max(1, std::min(4095, target / std::max(1, s.L)));
-        while (i < blocks.size() && (int)s.blk.size() < rmax && blocks[i].lg == s.lg && blocks[i].L == s.L)
-            s.blk.push_back(std::move(blocks[i++]));
-        sl.push_back(std::move(s));
     }
     // LPT: longest slice first onto the least-loaded warp (cost ≈ slots + slice overhead)
     std::vector<int> order(sl.size());
     std::iota(order.begin(), order.end(), 0);
-    auto slots_of = [&](const Slice &x) { return (long long)x.L * (long long)x.blk.size(); };
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return slots_of(sl[a]) > slots_of(sl[b]); });
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sl[a].L > sl[b].L; });
     using Item = std::pair<long long, int>;
     std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
     for (int w = 0; w < W; ++w) heap.push({0, w});
@@ -110,11 +92,9 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
         Item it = heap.top();
         heap.pop();
         wsl[it.second].push_back(q);
-        heap.push({it.first + slots_of(sl[q]) + 4 + 2 * (long long)sl[q].blk.size(), it.second});
+        heap.push({it.first + sl[q].L + 4, it.second});
     }
-    auto slice_bytes = [](const Slice &s) {
-        return (size_t)128 + s.blk.size() * ((size_t)128 + (size_t)(s.L / 2) * 384);
-    };
+    auto slice_bytes = [](const Slice &s) { return (size_t)128 + (size_t)(s.L / 2) * 384; };
     std::vector<int> warp_off(W), warp_nsl(W);
     size_t bytes = 0;
     int slots_max = 0;
@@ -122,7 +102,7 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
         warp_off[w] = (int)bytes;
         warp_nsl[w] = (int)wsl[w].size();
         int slots = 0;
-        for (int q : wsl[w]) { bytes += slice_bytes(sl[q]); slots += (int)slots_of(sl[q]); }
+        for (int q : wsl[w]) { bytes += slice_bytes(sl[q]); slots += sl[q].L; }
         slots_max = std::max(slots_max, slots);
     }
     if (bytes >= (size_t)1 << 31) return false;
@@ -138,25 +118,16 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     for (int w = 0; w < W; ++w) {
         size_t o = warp_off[w];
         for (int q : wsl[w]) {
-          const Slice &sx = sl[q];
-          const int R = (int)sx.blk.size();
-          {
-              int32_t *h0 = (int32_t *)(base + o);
-              for (int l = 0; l < 32; ++l)
-                  h0[l] = (int32_t)((uint32_t)sx.lg | ((uint32_t)(sx.L / 2) << 3) | ((uint32_t)R << 19));
-          }
-          int32_t *rowids = (int32_t *)(base + o + 128);
-          size_t ob = o + 128 + (size_t)R * 128;
-          for (int rb = 0; rb < R; ++rb) {
-            const Block &s = sx.blk[rb];
+            const Slice &s = sl[q];
             const int g = 1 << s.lg, L2 = s.L / 2;
-            uint32_t *idx = (uint32_t *)(base + ob);
-            float *wt = (float *)(base + ob + (size_t)L2 * 128);
+            int32_t *hdr = (int32_t *)(base + o);
+            uint32_t *idx = (uint32_t *)(base + o + 128);
+            float *wt = (float *)(base + o + 128 + (size_t)L2 * 128);
             for (int l = 0; l < 32; ++l) {
                 int ri = l >> s.lg, t = l & (g - 1);
                 bool has = ri < (int)s.rows.size();
                 uint32_t lead = (has && t == 0) ? (uint32_t)(s.rows[ri] + 1) : 0u;
-                rowids[rb * 32 + l] = (int32_t)lead;
+                hdr[l] = (int32_t)(lead | ((uint32_t)s.lg << 16) | ((uint32_t)L2 << 19));
                 rem[l].clear();
                 if (has) {
                     const int r = s.rows[ri];
@@ -268,7 +239,7 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
             if (Ls > 1 && mode == MODE_FACTORED) {
                 std::vector<int> rc(Ls);
                 for (int r = 0; r < Ls; ++r) rc[r] = row_cost(r);
-                uint64_t rng = 0x9E3779B97F4A7C15ull ^ ((uint64_t)q << 17) ^ ((uint64_t)rb << 40) ^ (uint64_t)Ls;
+                uint64_t rng = 0x9E3779B97F4A7C15ull ^ ((uint64_t)q << 17) ^ (uint64_t)Ls;
                 auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
                 const int iters = 60 * Ls * 32;
                 for (int it = 0; it < iters; ++it) {
@@ -302,9 +273,7 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
                     wt[((sl2 / 2) * 32 + l) * 2 + (sl2 & 1)] = wf;
                 }
             }
-            ob += (size_t)L2 * 384;
-          }
-          o += slice_bytes(sx);
+            o += slice_bytes(s);
         }
     }
     hs.rec_off.push_back((long long)off);

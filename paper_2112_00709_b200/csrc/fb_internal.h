@@ -28,15 +28,12 @@ enum Mode : int { MODE_FACTORED = 0, MODE_EXACT = 1,
 // are packed onto warps longest-first; every lane of a warp executes the same
 // instruction stream with no per-arc control flow.
 //
-// Byte layout of one slice: R blocks of 32/g rows with L arcs per lane each
-// (L even, null-padded):
-//   header  int32[32]        log2(g) | (L/2) << 3 | R << 19        (warp-uniform)
-//   rows    int32[R][32]     lane l of block r: row+1 if it leads a row, else 0
-//   then per block r:
+// Byte layout of one slice with L arcs per lane (L even, null-padded):
+//   header  int32[32]        lane l: (row+1 if l leads a row else 0) | log2(g) << 16 | (L/2) << 19
 //   index   uint32[L/2][32]  two u16 byte offsets of the other endpoints in the
 //                            gathered array (p in factored mode, u in exact mode);
 //                            slot 2i in the low half, 2i+1 in the high half
-//   weight  float2[L/2][32]  e^{T} (factored), T·log2(e) (exact) or T (Viterbi)
+//   weight  float2[L/2][32]  e^{T} (factored) or T·log2(e) (exact) for slots 2i, 2i+1
 // Member g's blob starts at byte rec_off[g] (rec_bytes[g] bytes); warp w's
 // slices start at byte warp_off[g*W+w] of the blob, warp_nsl[g*W+w] of them.
 struct Sched {

@@ -275,13 +275,13 @@ struct FBArgs {
 // Exact max-then-sum over one row held by g lanes (fallback of factored mode,
 // where weights are stored as e^{T}); `cur` is the slice, `lane` the group
 // leader.  Accurate libm ops; rare.
-__device__ __noinline__ float exact_row(uint32_t blk, int L2, int g, int lane, uint32_t a_u) {
+__device__ __noinline__ float exact_row(uint32_t cur, int L2, int g, int lane, uint32_t a_u) {
     float m = NEG_INF, sum = 0.f;
     for (int t = 0; t < g; ++t)
         for (int s = 0; s < 2 * L2; ++s) {
-            uint32_t ix = lds_u32(blk + (s >> 1) * 128 + (lane + t) * 4);
+            uint32_t ix = lds_u32(cur + 128 + (s >> 1) * 128 + (lane + t) * 4);
             uint32_t o = (s & 1) ? (ix >> 16) : (ix & 0xFFFFu);
-            float w = lds_v(blk + L2 * 128 + (s >> 1) * 256 + (lane + t) * 8 + (s & 1) * 4, 0.f);
+            float w = lds_v(cur + 128 + L2 * 128 + (s >> 1) * 256 + (lane + t) * 8 + (s & 1) * 4, 0.f);
             float x = lds_v(a_u + o, 0.f) + log2f(w);
             if (x == NEG_INF) continue;
             if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
@@ -303,64 +303,57 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
     constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
     constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
     constexpr uint32_t VS = sizeof(V);
-    const uint32_t l4 = (uint32_t)lane * 4, l8 = (uint32_t)lane * 8;
     for (int q = 0; q < nsl; ++q) {
-        const uint32_t h = lds_u32(cur + l4);
-        const int lg = (int)(h & 7u), L2 = (int)((h >> 3) & 0xFFFFu), R = (int)(h >> 19);
-        const uint32_t rows = cur + 128;
-        uint32_t blk = rows + (uint32_t)R * 128;
-        for (int r = 0; r < R; ++r) {
-            const int row = (int)lds_u32(rows + (uint32_t)r * 128 + l4) - 1;
-            uint32_t ia = blk + l4;
-            uint32_t wa = blk + (uint32_t)L2 * 128 + l8;
-            if (MODE == MODE_FACTORED) {
-                float a0 = 0.f, a1 = 0.f;
+        const uint32_t h = lds_u32(cur + lane * 4);
+        const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
+        uint32_t ia = cur + 128 + lane * 4;
+        uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
+        if (MODE == MODE_FACTORED) {
+            float a0 = 0.f, a1 = 0.f;
 #pragma unroll 2
-                for (int s = 0; s < L2; ++s) {
-                    const uint32_t ix = lds_u32(ia);
-                    const float2 w2 = lds_f2(wa);
-                    const float p0 = lds_v(a_p + (ix & 0xFFFFu), 0.f), p1 = lds_v(a_p + (ix >> 16), 0.f);
-                    a0 = fmaf(p0, w2.x, a0);
-                    a1 = fmaf(p1, w2.y, a1);
-                    ia += 128;
-                    wa += 256;
-                }
-                float acc = a0 + a1;
-                if (lg) {
-                    for (int o = 1; o < (1 << lg); o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                }
-                if (row >= 0)
-                    sts_v(a_part + (uint32_t)row * VS,
-                          (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(blk, L2, 1 << lg, lane, a_u)));
-            } else {
-                V m0 = ninf<V>(), m1 = ninf<V>();
-                float s0 = 0.f, s1 = 0.f;
-                auto push = [&](V &m, float &sm, uint32_t off, float w) {
-                    V x = lds_v(a_u + off, (V)0) + (V)w;
-                    V hi = vmax(m, x), lo = vmin(m, x);
-                    float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
-                    sm = (x > m) ? fmaf(sm, e, 1.f) : sm + e;
-                    m = hi;
-                };
-                for (int s = 0; s < L2; ++s) {
-                    const uint32_t ix = lds_u32(ia);
-                    const float2 w2 = lds_f2(wa);
-                    push(m0, s0, ix & 0xFFFFu, w2.x);
-                    push(m1, s1, ix >> 16, w2.y);
-                    ia += 128;
-                    wa += 256;
-                }
-                lse_combine(m0, s0, m1, s1);
-                for (int o = 1; o < (1 << lg); o <<= 1) {
-                    V m2 = __shfl_xor_sync(0xffffffffu, m0, o);
-                    float s2 = __shfl_xor_sync(0xffffffffu, s0, o);
-                    lse_combine(m0, s0, m2, s2);
-                }
-                if (row >= 0) sts_v(a_part + (uint32_t)row * VS, (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0));
+            for (int s = 0; s < L2; ++s) {
+                const uint32_t ix = lds_u32(ia);
+                const float2 w2 = lds_f2(wa);
+                const float p0 = lds_v(a_p + (ix & 0xFFFFu), 0.f), p1 = lds_v(a_p + (ix >> 16), 0.f);
+                a0 = fmaf(p0, w2.x, a0);
+                a1 = fmaf(p1, w2.y, a1);
+                ia += 128;
+                wa += 256;
             }
-            blk += (uint32_t)L2 * 384;
+            float acc = a0 + a1;
+            if (lg) {
+                for (int o = 1; o < (1 << lg); o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            }
+            if (row >= 0)
+                sts_v(a_part + (uint32_t)row * VS,
+                      (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(cur, L2, 1 << lg, lane, a_u)));
+        } else {
+            V m0 = ninf<V>(), m1 = ninf<V>();
+            float s0 = 0.f, s1 = 0.f;
+            auto push = [&](V &m, float &sm, uint32_t off, float w) {
+                V x = lds_v(a_u + off, (V)0) + (V)w;
+                V hi = vmax(m, x), lo = vmin(m, x);
+                float e = (lo == ninf<V>()) ? 0.f : ex2((float)(lo - hi));
+                sm = (x > m) ? fmaf(sm, e, 1.f) : sm + e;
+                m = hi;
+            };
+            for (int s = 0; s < L2; ++s) {
+                const uint32_t ix = lds_u32(ia);
+                const float2 w2 = lds_f2(wa);
+                push(m0, s0, ix & 0xFFFFu, w2.x);
+                push(m1, s1, ix >> 16, w2.y);
+                ia += 128;
+                wa += 256;
+            }
+            lse_combine(m0, s0, m1, s1);
+            for (int o = 1; o < (1 << lg); o <<= 1) {
+                V m2 = __shfl_xor_sync(0xffffffffu, m0, o);
+                float s2 = __shfl_xor_sync(0xffffffffu, s0, o);
+                lse_combine(m0, s0, m2, s2);
+            }
+            if (row >= 0) sts_v(a_part + (uint32_t)row * VS, (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0));
         }
-        cur = blk;
+        cur += 128 + (uint32_t)L2 * 384;
     }
 }
 
@@ -827,40 +820,33 @@ __device__ __forceinline__ void vit_consider(double &best, int &arg, double x, i
 
 __device__ __forceinline__ void phase_a_max(uint32_t cur, int nsl, int lane, uint32_t a_u, uint32_t a_best,
                                             uint32_t a_arg) {
-    const uint32_t l4 = (uint32_t)lane * 4, l8 = (uint32_t)lane * 8;
     for (int q = 0; q < nsl; ++q) {
-        const uint32_t h = lds_u32(cur + l4);
-        const int lg = (int)(h & 7u), L2 = (int)((h >> 3) & 0xFFFFu), R = (int)(h >> 19);
-        const uint32_t rows = cur + 128;
-        uint32_t blk = rows + (uint32_t)R * 128;
-        for (int r = 0; r < R; ++r) {
-            const int row = (int)lds_u32(rows + (uint32_t)r * 128 + l4) - 1;
-            uint32_t ia = blk + l4;
-            uint32_t wa = blk + (uint32_t)L2 * 128 + l8;
-            double b0 = NEG_INF_D, b1 = NEG_INF_D;
-            int g0 = 0x7fffffff, g1 = 0x7fffffff;
-            for (int s = 0; s < L2; ++s) {
-                const uint32_t ix = lds_u32(ia);
-                const float2 w2 = lds_f2(wa);
-                const uint32_t o0 = ix & 0xFFFFu, o1 = ix >> 16;
-                vit_consider(b0, g0, lds_v(a_u + o0, 0.0) + (double)w2.x, (int)(o0 >> 3));
-                vit_consider(b1, g1, lds_v(a_u + o1, 0.0) + (double)w2.y, (int)(o1 >> 3));
-                ia += 128;
-                wa += 256;
-            }
-            vit_consider(b0, g0, b1, g1);
-            for (int o = 1; o < (1 << lg); o <<= 1) {
-                const double bo = __shfl_xor_sync(0xffffffffu, b0, o);
-                const int go = __shfl_xor_sync(0xffffffffu, g0, o);
-                vit_consider(b0, g0, bo, go);
-            }
-            if (row >= 0) {
-                sts_v(a_best + (uint32_t)row * 8, b0);
-                sts_i(a_arg + (uint32_t)row * 4, b0 == NEG_INF_D ? -1 : g0);
-            }
-            blk += (uint32_t)L2 * 384;
+        const uint32_t h = lds_u32(cur + lane * 4);
+        const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
+        uint32_t ia = cur + 128 + lane * 4;
+        uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
+        double b0 = NEG_INF_D, b1 = NEG_INF_D;
+        int g0 = 0x7fffffff, g1 = 0x7fffffff;
+        for (int s = 0; s < L2; ++s) {
+            const uint32_t ix = lds_u32(ia);
+            const float2 w2 = lds_f2(wa);
+            const uint32_t o0 = ix & 0xFFFFu, o1 = ix >> 16;
+            vit_consider(b0, g0, lds_v(a_u + o0, 0.0) + (double)w2.x, (int)(o0 >> 3));
+            vit_consider(b1, g1, lds_v(a_u + o1, 0.0) + (double)w2.y, (int)(o1 >> 3));
+            ia += 128;
+            wa += 256;
         }
-        cur = blk;
+        vit_consider(b0, g0, b1, g1);
+        for (int o = 1; o < (1 << lg); o <<= 1) {
+            const double bo = __shfl_xor_sync(0xffffffffu, b0, o);
+            const int go = __shfl_xor_sync(0xffffffffu, g0, o);
+            vit_consider(b0, g0, bo, go);
+        }
+        if (row >= 0) {
+            sts_v(a_best + (uint32_t)row * 8, b0);
+            sts_i(a_arg + (uint32_t)row * 4, b0 == NEG_INF_D ? -1 : g0);
+        }
+        cur += 128 + (uint32_t)L2 * 384;
     }
 }
 

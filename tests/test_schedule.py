@@ -64,36 +64,31 @@ def decode(L, h, which, G, W, exact):
             woff, nsl = meta[2 * G + 2 * (g * W + w)], meta[2 * G + 2 * (g * W + w) + 1]
             cur = off + woff
             for _ in range(nsl):
-                hdr = blob[cur:cur + 128].view(np.int32).astype(np.int64) & 0xFFFFFFFF
-                lg = int(hdr[0] & 7)
-                L2 = int((hdr[0] >> 3) & 0xFFFF)
-                R = int(hdr[0] >> 19)
-                assert (hdr == hdr[0]).all()  # uniform
-                rowids = blob[cur + 128:cur + 128 + R * 128].view(np.int32).reshape(R, 32)
-                blk = cur + 128 + R * 128
-                for r in range(R):
-                    idx = blob[blk:blk + L2 * 128].view(np.uint32).reshape(L2, 32)
-                    wt = blob[blk + L2 * 128:blk + L2 * 384].view(np.float32).reshape(L2, 32, 2)
-                    gsz = 1 << lg
-                    for lane in range(32):
-                        lead = int(rowids[r, lane]) - 1
-                        if lead < 0:
-                            continue
-                        assert lane % gsz == 0
-                        arcs = []
-                        for t in range(lane, lane + gsz):
-                            for s in range(2 * L2):
-                                word = int(idx[s // 2, t])
-                                o = (word >> 16) if (s & 1) else (word & 0xFFFF)
-                                wv = float(wt[s // 2, t, s & 1])
-                                if wv == pad:
-                                    continue
-                                assert o % esize == 0
-                                arcs.append((o // esize, wv))
-                        assert lead not in rows[g], "row written twice"
-                        rows[g][lead] = Counter(arcs)
-                    blk += L2 * 384
-                cur = blk
+                hdr = blob[cur:cur + 128].view(np.int32)
+                lg = (hdr[0] >> 16) & 7
+                L2 = int(np.uint32(hdr[0]) >> 19)
+                assert ((hdr >> 16) & 7 == lg).all() and (np.uint32(hdr) >> 19 == L2).all()  # uniform
+                idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint32).reshape(L2, 32)
+                wt = blob[cur + 128 + L2 * 128:cur + 128 + L2 * 384].view(np.float32).reshape(L2, 32, 2)
+                gsz = 1 << lg
+                for lane in range(32):
+                    lead = (hdr[lane] & 0xFFFF) - 1
+                    if lead < 0:
+                        continue
+                    assert lane % gsz == 0
+                    arcs = []
+                    for t in range(lane, lane + gsz):
+                        for s in range(2 * L2):
+                            word = int(idx[s // 2, t])
+                            o = (word >> 16) if (s & 1) else (word & 0xFFFF)
+                            wv = float(wt[s // 2, t, s & 1])
+                            if wv == pad:
+                                continue
+                            assert o % esize == 0
+                            arcs.append((o // esize, wv))
+                    assert lead not in rows[g], "row written twice"
+                    rows[g][lead] = Counter(arcs)
+                cur += 128 + L2 * 384
             assert cur <= off + nbytes
     return rows
 
@@ -182,17 +177,13 @@ def test_bank_conflicts_reduced(L):
     for w in range(W):
         cur, nsl = meta[2 + 2 * w], meta[2 + 2 * w + 1]
         for _ in range(nsl):
-            h = int(np.uint32(blob[cur:cur + 4].view(np.int32)[0]))
-            L2, R = (h >> 3) & 0xFFFF, h >> 19
-            blk = cur + 128 + R * 128
-            for r in range(R):
-                idx = blob[blk:blk + L2 * 128].view(np.uint32).reshape(L2, 32)
-                for half in (idx & 0xFFFF, idx >> 16):
-                    for row in half:
-                        # wavefronts = most distinct addresses in one bank (equal addresses broadcast)
-                        banks = Counter((a // 4) % 32 for a in set(row.tolist()))
-                        tot += max(banks.values())
-                        rows += 1
-                blk += L2 * 384
-            cur = blk
+            L2 = int(np.uint32(blob[cur:cur + 4].view(np.int32)[0]) >> 19)
+            idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint32).reshape(L2, 32)
+            for half in (idx & 0xFFFF, idx >> 16):
+                for r in half:
+                    # wavefronts = most distinct addresses in one bank (equal addresses broadcast)
+                    banks = Counter((a // 4) % 32 for a in set(r.tolist()))
+                    tot += max(banks.values())
+                    rows += 1
+            cur += 128 + L2 * 384
     assert tot / rows < 2.1, tot / rows  # unordered placement averages ~2.6-way
