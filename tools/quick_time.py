@@ -11,7 +11,7 @@ import paper_2112_00709_b200 as fbx
 from paper_2112_00709_b200 import synth
 
 
-def timeit(fn, reps=5, warm=2):
+def timeit(fn, reps=20, warm=3):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -38,8 +38,10 @@ if "c3" in which:
         logZ, _, _, st = fbx.fb_forward(g, e, L, alpha=alpha, alpha_scale=sc)
         fbx.fb_backward(g, e, L, alpha=alpha, status=st, post="state", post_out=post)
     ms = timeit(step)
-    fbx.profile_enable(True); fbx.profile_reset(); step(); torch.cuda.synchronize()
-    print("profile", fbx.profile_collect()); fbx.profile_enable(False)
+    fbx.profile_enable(True); fbx.profile_reset()
+    for _ in range(10): step()
+    torch.cuda.synchronize()
+    print("profile", {k: round(v[1] / v[0], 4) for k, v in fbx.profile_collect().items()}); fbx.profile_enable(False)
     print(f"C3 fwd+bwd+post: {ms:.3f} ms  -> {64000/ms*1e3:.3e} seq-frames/s", flush=True)
     del alpha, post, e
 if "c4" in which:
@@ -55,6 +57,8 @@ if "c4" in which:
     st = torch.empty(128, dtype=torch.int32, device="cuda")
     step = lambda: fbx.lfmmi_loss_grad(num, den, e, L, grad, ws, loss, tot, st)
     ms = timeit(step)
-    fbx.profile_enable(True); fbx.profile_reset(); step(); torch.cuda.synchronize()
-    print("profile", fbx.profile_collect()); fbx.profile_enable(False)
+    fbx.profile_enable(True); fbx.profile_reset()
+    for _ in range(10): step()
+    torch.cuda.synchronize()
+    print("profile", {k: round(v[1] / v[0], 4) for k, v in fbx.profile_collect().items()}); fbx.profile_enable(False)
     print(f"C4 lfmmi: {ms:.3f} ms  -> {64000/ms*1e3:.3e} seq-frames/s  totals {tot.cpu().numpy()}", flush=True)
