@@ -94,22 +94,15 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
         wsl[it.second].push_back(q);
         heap.push({it.first + sl[q].L + 4, it.second});
     }
-    // Factored mode uses the "stream" layout: a warp's slices concatenated into
-    // one run of P arc pairs (idx u32[P][32] | weight float2[P][32] | flush
-    // int32[F][32]) with each slice's end marked by the sign bit of the .y
-    // weight of its last pair in every lane (weights e^T ≥ 0).  Other modes use
-    // one header + block per slice.
-    const bool stream = mode == MODE_FACTORED;
     auto slice_bytes = [](const Slice &s) { return (size_t)128 + (size_t)(s.L / 2) * 384; };
-    std::vector<int> warp_off(W), warp_nsl(W), warp_pairs(W);
+    std::vector<int> warp_off(W), warp_nsl(W);
     size_t bytes = 0;
     int slots_max = 0;
     for (int w = 0; w < W; ++w) {
         warp_off[w] = (int)bytes;
+        warp_nsl[w] = (int)wsl[w].size();
         int slots = 0;
         for (int q : wsl[w]) { bytes += slice_bytes(sl[q]); slots += sl[q].L; }
-        warp_pairs[w] = slots / 2;
-        warp_nsl[w] = stream ? slots / 2 : (int)wsl[w].size();
         slots_max = std::max(slots_max, slots);
     }
     if (bytes >= (size_t)1 << 31) return false;
@@ -124,21 +117,17 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     std::vector<std::vector<long long>> rem(32);
     for (int w = 0; w < W; ++w) {
         size_t o = warp_off[w];
-        const size_t P = (size_t)warp_pairs[w];
-        size_t po = 0, fi = 0;  // stream layout: pair and flush cursors
         for (int q : wsl[w]) {
             const Slice &s = sl[q];
             const int g = 1 << s.lg, L2 = s.L / 2;
-            int32_t *hdr = stream ? (int32_t *)(base + warp_off[w] + P * 384 + fi * 128) : (int32_t *)(base + o);
-            uint32_t *idx = stream ? (uint32_t *)(base + warp_off[w] + po * 128) : (uint32_t *)(base + o + 128);
-            float *wt = stream ? (float *)(base + warp_off[w] + P * 128 + po * 256)
-                               : (float *)(base + o + 128 + (size_t)L2 * 128);
+            int32_t *hdr = (int32_t *)(base + o);
+            uint32_t *idx = (uint32_t *)(base + o + 128);
+            float *wt = (float *)(base + o + 128 + (size_t)L2 * 128);
             for (int l = 0; l < 32; ++l) {
                 int ri = l >> s.lg, t = l & (g - 1);
                 bool has = ri < (int)s.rows.size();
                 uint32_t lead = (has && t == 0) ? (uint32_t)(s.rows[ri] + 1) : 0u;
-                hdr[l] = stream ? (int32_t)(lead | ((uint32_t)s.lg << 16))
-                                : (int32_t)(lead | ((uint32_t)s.lg << 16) | ((uint32_t)L2 << 19));
+                hdr[l] = (int32_t)(lead | ((uint32_t)s.lg << 16) | ((uint32_t)L2 << 19));
                 rem[l].clear();
                 if (has) {
                     const int r = s.rows[ri];
@@ -283,14 +272,6 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
                     word |= (sl2 & 1) ? (boff << 16) : boff;
                     wt[((sl2 / 2) * 32 + l) * 2 + (sl2 & 1)] = wf;
                 }
-            }
-            if (stream) {  // slice end marker: sign bit of the last pair's .y weight, every lane
-                for (int l = 0; l < 32; ++l) {
-                    float &y = wt[((size_t)(L2 - 1) * 32 + l) * 2 + 1];
-                    y = -std::fabs(y);
-                }
-                po += (size_t)L2;
-                ++fi;
             }
             o += slice_bytes(s);
         }

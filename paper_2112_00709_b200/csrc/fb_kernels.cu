@@ -290,65 +290,6 @@ __device__ __noinline__ float exact_row(uint32_t cur, int L2, int g, int lane, u
     return m == NEG_INF ? NEG_INF : m + log2f(sum);
 }
 
-// Exact max-then-sum over one row of the stream layout held by g lanes starting
-// at the calling (leader) lane: np pairs from idx / weight addresses ia0 / wa0
-// (already offset by the leader's lane).  Weights are e^{T} (sign = marker).
-__device__ __noinline__ float exact_row_stream(uint32_t ia0, uint32_t wa0, int np, int g, uint32_t a_u) {
-    float m = NEG_INF, sum = 0.f;
-    for (int t = 0; t < g; ++t)
-        for (int s = 0; s < 2 * np; ++s) {
-            const uint32_t ix = lds_u32(ia0 + (uint32_t)(s >> 1) * 128 + (uint32_t)t * 4);
-            const uint32_t o = (s & 1) ? (ix >> 16) : (ix & 0xFFFFu);
-            const float w = fabsf(lds_v(wa0 + (uint32_t)(s >> 1) * 256 + (uint32_t)t * 8 + (s & 1) * 4, 0.f));
-            const float x = lds_v(a_u + o, 0.f) + log2f(w);
-            if (x == NEG_INF) continue;
-            if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
-            else sum += exp2f(x - m);
-        }
-    return m == NEG_INF ? NEG_INF : m + log2f(sum);
-}
-
-// Factored phase A over the stream layout: this warp's P arc pairs in one run;
-// a slice ends where the .y weight carries the sign bit (warp-uniform), and
-// then the row values are combined / flushed (flush info int32 per lane:
-// row+1 | log2(g) << 16).
-__device__ __forceinline__ void phase_a_stream(uint32_t base, int P, int lane, uint32_t a_u, uint32_t a_p,
-                                               uint32_t a_part) {
-    constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
-    constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
-    uint32_t ia = base + (uint32_t)lane * 4;
-    uint32_t wa = base + (uint32_t)P * 128 + (uint32_t)lane * 8;
-    uint32_t fa = base + (uint32_t)P * 384 + (uint32_t)lane * 4;
-    uint32_t ia0 = ia, wa0 = wa;
-    int s0 = 0;
-    float a0 = 0.f, a1 = 0.f;
-#pragma unroll 2
-    for (int s = 0; s < P; ++s) {
-        const uint32_t ix = lds_u32(ia);
-        const float2 w2 = lds_f2(wa);
-        const float p0 = lds_v(a_p + (ix & 0xFFFFu), 0.f), p1 = lds_v(a_p + (ix >> 16), 0.f);
-        a0 = fmaf(p0, w2.x, a0);
-        a1 = fmaf(p1, fabsf(w2.y), a1);
-        ia += 128;
-        wa += 256;
-        if (__float_as_int(w2.y) < 0) {  // end of a slice (same slot in every lane)
-            const uint32_t fi = lds_u32(fa);
-            fa += 128;
-            const int lg = (int)((fi >> 16) & 7u), row = (int)(fi & 0xFFFFu) - 1;
-            float acc = a0 + a1;
-            for (int o = 1; o < (1 << lg); o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (row >= 0)
-                sts_v(a_part + (uint32_t)row * 4,
-                      (acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row_stream(ia0, wa0, s + 1 - s0, 1 << lg, a_u));
-            a0 = 0.f;
-            a1 = 0.f;
-            ia0 = ia;
-            wa0 = wa;
-            s0 = s + 1;
-        }
-    }
-}
-
 // Phase A: walk this warp's slices (layout: fb_internal.h, Sched).  Lane l
 // reduces one row segment per slice; the g lanes of a split row are combined
 // with a uniform xor-shuffle and the group leader writes the row's log2 value
@@ -763,8 +704,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         tma_issue(tstep + 1, n_next + dir);  // buffer of step tstep-1 is free now
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
         if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pslot, gi, b, pend_n, tid, T);
-        if constexpr (MODE == MODE_FACTORED) phase_a_stream(mysl, nsl, lane, a_u, a_p, a_part);
-        else phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
+        phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
         __syncthreads();
         // ---- phase B of frame n_next
         const int pp = par;

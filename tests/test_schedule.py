@@ -63,41 +63,6 @@ def decode(L, h, which, G, W, exact):
         for w in range(W):
             woff, nsl = meta[2 * G + 2 * (g * W + w)], meta[2 * G + 2 * (g * W + w) + 1]
             cur = off + woff
-            if not exact:  # factored: stream layout (one run of P pairs, sign-marked slice ends)
-                P = nsl
-                idx = blob[cur:cur + P * 128].view(np.uint32).reshape(P, 32)
-                wt = blob[cur + P * 128:cur + P * 384].view(np.float32).reshape(P, 32, 2)
-                fl = blob[cur + P * 384:].view(np.int32)
-                s0, f = 0, 0
-                for sp in range(P):
-                    neg = np.signbit(wt[sp, :, 1])
-                    assert neg.all() or not neg.any()  # marker is warp-uniform
-                    if not neg.all():
-                        continue
-                    info = fl[f * 32:(f + 1) * 32]
-                    lg = int(info[0] >> 16) & 7
-                    gsz = 1 << lg
-                    for lane in range(32):
-                        lead = int(info[lane] & 0xFFFF) - 1
-                        if lead < 0:
-                            continue
-                        assert lane % gsz == 0
-                        arcs = []
-                        for t in range(lane, lane + gsz):
-                            for q in range(s0, sp + 1):
-                                for half in (0, 1):
-                                    word = int(idx[q, t])
-                                    o = (word >> 16) if half else (word & 0xFFFF)
-                                    wv = abs(float(wt[q, t, half]))
-                                    if wv == 0.0:
-                                        continue
-                                    assert o % esize == 0
-                                    arcs.append((o // esize, wv))
-                        assert lead not in rows[g], "row written twice"
-                        rows[g][lead] = Counter(arcs)
-                    s0, f = sp + 1, f + 1
-                assert s0 == P
-                continue
             for _ in range(nsl):
                 hdr = blob[cur:cur + 128].view(np.int32)
                 lg = (hdr[0] >> 16) & 7
@@ -210,12 +175,15 @@ def test_bank_conflicts_reduced(L):
     W = int(info[4]) // 32
     tot = rows = 0
     for w in range(W):
-        cur, P = meta[2 + 2 * w], meta[2 + 2 * w + 1]
-        idx = blob[cur:cur + P * 128].view(np.uint32).reshape(P, 32)
-        for half in (idx & 0xFFFF, idx >> 16):
-            for row in half:
-                # wavefronts = most distinct addresses in one bank (equal addresses broadcast)
-                banks = Counter((a // 4) % 32 for a in set(row.tolist()))
-                tot += max(banks.values())
-                rows += 1
+        cur, nsl = meta[2 + 2 * w], meta[2 + 2 * w + 1]
+        for _ in range(nsl):
+            L2 = int(np.uint32(blob[cur:cur + 4].view(np.int32)[0]) >> 19)
+            idx = blob[cur + 128:cur + 128 + L2 * 128].view(np.uint32).reshape(L2, 32)
+            for half in (idx & 0xFFFF, idx >> 16):
+                for r in half:
+                    # wavefronts = most distinct addresses in one bank (equal addresses broadcast)
+                    banks = Counter((a // 4) % 32 for a in set(r.tolist()))
+                    tot += max(banks.values())
+                    rows += 1
+            cur += 128 + L2 * 384
     assert tot / rows < 2.1, tot / rows  # unordered placement averages ~2.6-way
