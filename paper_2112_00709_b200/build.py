@@ -8,13 +8,16 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfb.so")
-SOURCES = ["fb_graph.cpp", "fb_kernels.cu"]
-HEADERS = ["fb_internal.h", os.path.join("..", "..", "include", "fb.h")]
+SOURCES = ["fb_graph.cpp", "fb_kernels.cu", "fb_inst.cu"]
+# fb_inst.cu is compiled once per (direction, mode): the k_fb instantiation sets
+INST = [(bwd, mode) for bwd in (0, 1) for mode in (0, 1, 2, 4)]
+HEADERS = ["fb_internal.h", "fb_device.cuh", os.path.join("..", "..", "include", "fb.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
@@ -27,18 +30,28 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _units():
+    """(source, object, extra flags) of every translation unit."""
+    units = [("fb_graph.cpp", "fb_graph.o", []), ("fb_kernels.cu", "fb_kernels.o", [])]
+    units += [("fb_inst.cu", f"fb_inst_b{b}_m{m}.o", [f"-DFBX_BWD={b}", f"-DFBX_MODE={m}"]) for b, m in INST]
+    return units
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objs = []
-    for src in SOURCES:
-        obj = os.path.join(CSRC, src + ".o")
+    cmds, objs = [], []
+    for src, obj, extra in _units():
+        obj = os.path.join(CSRC, obj)
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
-               "-c", os.path.join(CSRC, src), "-o", obj]
-        if src.endswith(".cu"):
-            cmd[1:1] = ["-Xptxas", "-v"] if verbose else []
-        subprocess.check_call(cmd)
+               *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        if src.endswith(".cu") and verbose:
+            cmd[1:1] = ["-Xptxas", "-v"]
+        cmds.append(cmd)
         objs.append(obj)
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
+            f.result()
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-lpthread"])
     os.replace(tmp, LIB)

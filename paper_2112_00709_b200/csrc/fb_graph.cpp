@@ -505,7 +505,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.pm.U_tot = slot_off[G];
     if (gr.pm.U_max >= 32768 || (long long)D * 2 > 65536) return FB_ERR_UNSUPPORTED;  // i16 pdf maps in smem
     if (smem_bytes(gr, false, false) > (size_t)kSmemLimit ||
-        smem_bytes(gr, true, true) + pdf_region(POST_GRAD, gr.pm.U_max, D).bytes > (size_t)kSmemLimit)
+        smem_bytes(gr, true, true) + std::max(pdf_region(POST_GRAD, gr.pm.U_max, D).bytes,
+                                              pdf_region(POST_PDF_COMPACT, gr.pm.U_max, D).bytes) >
+            (size_t)kSmemLimit)
         return FB_ERR_UNSUPPORTED;
 
     // pack and upload

@@ -118,16 +118,17 @@ FBX_HD inline SmemLayout smem_layout(int rec_bytes, int K_pad, bool exact, bool 
 enum PostKind : int { POST_NONE = 0, POST_STATE = 1, POST_PDF_DENSE = 2, POST_PDF_COMPACT = 3, POST_GRAD = 4 };
 
 // Shared-memory region of the pdf-level epilogue, placed after the reductions:
-// ssp   u16[U+1]  slot boundaries of the member's slot-ordered state list
-// pslot i16[D]    pdf → slot (-1 unused)            (dense / grad)
+// ssp u16[U+1]  slot boundaries of the member's slot-ordered state list  (compact)
+// pq  u32[D]    pdf → q0 | count << 16: its states' run in the slot-ordered
+//               γ row (count 0: pdf unused)                          (dense / grad)
 struct PdfRegion {
-    size_t ssp, pslot, bytes;
+    size_t ssp, pq, bytes;
 };
 FBX_HD inline PdfRegion pdf_region(int kind, int U_max, int D) {
     PdfRegion R;
     size_t o = 0;
-    R.ssp = o; o += fbx_a16((size_t)(U_max + 1) * 2);
-    R.pslot = o; if (kind == POST_PDF_DENSE || kind == POST_GRAD) o += fbx_a16((size_t)D * 2);
+    R.ssp = o; if (kind == POST_PDF_COMPACT) o += fbx_a16((size_t)(U_max + 1) * 2);
+    R.pq = o; if (kind == POST_PDF_DENSE || kind == POST_GRAD) o += fbx_a16((size_t)D * 4);
     R.bytes = (kind == POST_PDF_DENSE || kind == POST_PDF_COMPACT || kind == POST_GRAD) ? o : 0;
     return R;
 }
