@@ -74,6 +74,10 @@ enum {
     FB_GRAPH_DEFAULT = 0,
     FB_GRAPH_FORCE_EXACT = 1,    /* every ⊕ row evaluated max-then-sum (one exp per arc) */
     FB_GRAPH_FORCE_FACTORED = 2, /* exp-factorised ⊕ with exact fallback */
+    FB_GRAPH_CLUSTER = 4,        /* shared (G = 1) factored graphs: run the cluster-batched kernel
+                                    (C CTAs × S sequences per thread-block cluster) even when one
+                                    sequence's schedule fits one SM; graphs that do not fit one SM
+                                    (e.g. the paper's 50,984-arc denominator) always use it */
     FB_GRAPH_DRY_RUN = 256       /* run the host compiler only: no device allocation; the handle
                                     supports fb_graph_info/destroy, compute calls reject it */
 };
@@ -121,7 +125,9 @@ fb_status fb_graph_destroy(fb_graph g);
 /*
  * fb_graph_info — [host] out[16] int64: {G, K_tot, nnz, D, threads_per_cta,
  * states_per_thread, mode (0 factored / 1 exact / 2 mixed), fwd_smem_bytes,
- * bwd_smem_bytes, K_max, nnz_max, fwd_slots_max, bwd_slots_max, U_max, 0, 0}.
+ * bwd_smem_bytes, K_max, nnz_max, fwd_slots_max, bwd_slots_max, U_max,
+ * cluster_C, cluster_S}: cluster_C > 0 when a shared factored graph runs the
+ * cluster-batched kernel (C CTAs per cluster, S sequences per cluster).
  */
 fb_status fb_graph_info(fb_graph g, int64_t *out);
 

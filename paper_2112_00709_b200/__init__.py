@@ -27,11 +27,11 @@ __all__ = [
     "FBError", "Graph", "fb_forward", "fb_backward", "fb_posteriors", "lfmmi_loss_grad", "workspace_bytes",
     "fb_viterbi", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
     "SEQ_OK", "SEQ_EMPTY_LATTICE", "SEQ_NONFINITE_INPUT", "SEQ_BAD_LENGTH",
-    "GRAPH_DEFAULT", "GRAPH_FORCE_EXACT", "GRAPH_FORCE_FACTORED",
+    "GRAPH_DEFAULT", "GRAPH_FORCE_EXACT", "GRAPH_FORCE_FACTORED", "GRAPH_CLUSTER",
 ]
 
 SEQ_OK, SEQ_EMPTY_LATTICE, SEQ_NONFINITE_INPUT, SEQ_BAD_LENGTH = 0, 1, 2, 4
-GRAPH_DEFAULT, GRAPH_FORCE_EXACT, GRAPH_FORCE_FACTORED = 0, 1, 2
+GRAPH_DEFAULT, GRAPH_FORCE_EXACT, GRAPH_FORCE_FACTORED, GRAPH_CLUSTER = 0, 1, 2, 4
 
 
 class FBError(RuntimeError):
@@ -96,7 +96,7 @@ class Graph:
         info = np.zeros(16, np.int64)
         _check(lib().fb_graph_info(h, _np_ptr(info)), "fb_graph_info")
         keys = ["G", "K_tot", "nnz", "D", "threads", "spt", "mode", "fwd_smem", "bwd_smem", "K_max", "nnz_max",
-                "fwd_slots_max", "bwd_slots_max", "U_max"]
+                "fwd_slots_max", "bwd_slots_max", "U_max", "cluster_C", "cluster_S"]
         self.info = {k: int(v) for k, v in zip(keys, info)}
         self.K_tot = self.info["K_tot"]
 

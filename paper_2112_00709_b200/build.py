@@ -14,9 +14,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfb.so")
-SOURCES = ["fb_graph.cpp", "fb_kernels.cu", "fb_inst.cu"]
+SOURCES = ["fb_graph.cpp", "fb_kernels.cu", "fb_inst.cu", "fb_cluster.cu"]
 # fb_inst.cu is compiled once per (direction, mode): the k_fb instantiation sets
 INST = [(bwd, mode) for bwd in (0, 1) for mode in (0, 1, 2, 4)]
+# fb_cluster.cu once per (direction, sequences per cluster)
+CINST = [(bwd, s) for bwd in (0, 1) for s in (2, 4)]
 HEADERS = ["fb_internal.h", "fb_device.cuh", os.path.join("..", "..", "include", "fb.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -34,6 +36,7 @@ def _units():
     """(source, object, extra flags) of every translation unit."""
     units = [("fb_graph.cpp", "fb_graph.o", []), ("fb_kernels.cu", "fb_kernels.o", [])]
     units += [("fb_inst.cu", f"fb_inst_b{b}_m{m}.o", [f"-DFBX_BWD={b}", f"-DFBX_MODE={m}"]) for b, m in INST]
+    units += [("fb_cluster.cu", f"fb_cluster_b{b}_s{s}.o", [f"-DFBX_BWD={b}", f"-DFBX_S={s}"]) for b, s in CINST]
     return units
 
 

@@ -1,0 +1,697 @@
+// fb_cluster.cu — cluster-batched forward / backward recursion k_fbc for a
+// shared (G == 1) factored graph (the LF-MMI denominator).
+//
+// One thread-block cluster of C CTAs runs S sequences in lockstep, frame by
+// frame (batched as P:193-227).  The graph's states are split into C
+// parts along pdf ranges (CPlan, fb_internal.h); CTA c owns part c and, per
+// frame, computes its rows for all S sequences:
+//
+//   wait      mbarrier: the other parts' rows u_{t−1} (log2, normalised) and
+//             their per-sequence extras (max, posterior normaliser partials)
+//             have landed in this CTA's shared memory (bulk DSMEM copies)
+//   convert   p = 2^u for the received rows (one ex2 per element)
+//   barrier
+//   posterior γ_{t−1} = 2^{x − Z} (backward; Z = LSE over all parts, Eq. (15))
+//   phase A   the part's sliced-ELL rows: Σ_src p[src][0..S) · e^{T} — one
+//             S-wide vector gather and S FMAs per arc (the arc record is read
+//             once for S sequences)
+//   barrier
+//   pdf rows  Γ / −Γ_den of frame t−1 for the part's pdf range (part-local)
+//   phase B   y = log2 Σ (exact max-then-sum fallback outside [2^-80, 2^120]),
+//             emission, lagged per-sequence normaliser c_t = max u_{t−1}
+//             (SURVEY §8(c4)), α̂/β̂ to HBM, new u and p of the part's rows
+//   barrier
+//   send      the part's u rows + extras to the C−1 other CTAs
+//             (cp.async.bulk shared::cta → shared::cluster, complete_tx on the
+//             receiver's mbarrier; double-buffered u, so no cluster barrier)
+//
+// Emission segments (the part's pdf range of each φ row) are staged with
+// cp.async one frame ahead.  Per-sequence results are independent of the other
+// sequences of the cluster (no cross-sequence arithmetic).
+#include "fb_device.cuh"
+
+#if !defined(FBX_BWD) || !defined(FBX_S)
+#error "compile with -DFBX_BWD=<0|1> -DFBX_S=<2|4>"
+#endif
+
+namespace fbx {
+
+__device__ __forceinline__ uint32_t cl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cl_id() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float cl_ldf(uint32_t a) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void bulk_s2s(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "r"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAITC_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+        " @!P1 bra WAITC_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void cpa16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa4(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// S-float vectors in shared memory
+template <int S>
+struct VS;
+template <>
+struct VS<2> {
+    static __device__ __forceinline__ void ld(uint32_t a, float *v) {
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[0]), "=f"(v[1]) : "r"(a));
+    }
+    static __device__ __forceinline__ void st(uint32_t a, const float *v) {
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v[0]), "f"(v[1]));
+    }
+};
+template <>
+struct VS<4> {
+    static __device__ __forceinline__ void ld(uint32_t a, float *v) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]) : "r"(a));
+    }
+    static __device__ __forceinline__ void st(uint32_t a, const float *v) {
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]));
+    }
+};
+
+// Phase A over this warp's slices (Sched layout, fb_internal.h) with S-float
+// gathered elements: lane l reduces one row segment for all S sequences.
+template <int S>
+__device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uint32_t a_p, uint32_t a_part) {
+    for (int q = 0; q < nsl; ++q) {
+        const uint32_t h = lds_u32(cur + lane * 4);
+        const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
+        uint32_t ia = cur + 128 + lane * 4;
+        uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
+        float a0[S], a1[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i) { a0[i] = 0.f; a1[i] = 0.f; }
+#pragma unroll 2
+        for (int s = 0; s < L2; ++s) {
+            const uint32_t ix = lds_u32(ia);
+            const float2 w2 = lds_f2(wa);
+            float p0[S], p1[S];
+            VS<S>::ld(a_p + (ix & 0xFFFFu), p0);
+            VS<S>::ld(a_p + (ix >> 16), p1);
+#pragma unroll
+            for (int i = 0; i < S; ++i) {
+                a0[i] = fmaf(p0[i], w2.x, a0[i]);
+                a1[i] = fmaf(p1[i], w2.y, a1[i]);
+            }
+            ia += 128;
+            wa += 256;
+        }
+        float acc[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i) acc[i] = a0[i] + a1[i];
+        for (int o = 1; o < (1 << lg); o <<= 1) {
+#pragma unroll
+            for (int i = 0; i < S; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+        }
+        if (row >= 0) VS<S>::st(a_part + (uint32_t)row * (S * 4), acc);
+        cur += 128 + (uint32_t)L2 * 384;
+    }
+}
+
+// Exact max-then-sum of one row for sequence s over the previous frame's u
+// (fallback of the factored sum; accurate libm ops; rare).
+template <int S>
+static __device__ __noinline__ float exact_row_c(const int *ptr, const int *src, const float *w2, int row, int s,
+                                                 uint32_t a_uprev) {
+    float m = NEG_INF, sum = 0.f;
+    for (int e = ptr[row]; e < ptr[row + 1]; ++e) {
+        const float x = lds_v(a_uprev + (uint32_t)(src[e] * S + s) * 4, 0.f) + w2[e];
+        if (x == NEG_INF) continue;
+        if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
+        else sum += exp2f(x - m);
+    }
+    return m == NEG_INF ? NEG_INF : m + log2f(sum);
+}
+
+// Combine (m, s) log-sum-exp pairs (m in log2, s ≥ 0) in a fixed order.
+__device__ __forceinline__ void lse2(float &m, float &s, float m2, float s2) { lse_combine<float>(m, s, m2, s2); }
+
+template <bool BWD, int S, int SPT, int T>
+__global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int W = T / 32;
+    constexpr float kTiny = 8.271806125530277e-25f, kHuge = 1.329227995784916e+36f;  // 2^-80, 2^120
+    const Graph &G = a.g;
+    const CPlan &P = G.cp;
+    const int C = P.C;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int cr = (int)cl_rank();
+    const int grp = (int)cl_id();
+    const int K = G.K_tot, Kint = P.K_int, D = a.D, N_max = a.N_max;
+    const int k0 = P.part_off[cr], Kc = P.part_off[cr + 1] - k0;
+    const Sched &SC = BWD ? P.bwd : P.fwd;
+    const bool want_post = BWD && a.post_kind != POST_NONE;
+    const bool pdf_post = want_post && a.post_kind != POST_STATE;
+    const CLayout L = cl_layout(SC.bytes_max, Kint, P.Kc_max, P.Dc_max, S, C, W, BWD);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t a_rec = sb + (uint32_t)L.rec, a_u0 = sb + (uint32_t)L.u, a_p = sb + (uint32_t)L.p;
+    const uint32_t a_part = sb + (uint32_t)L.part, a_gbuf = sb + (uint32_t)L.gbuf, a_pq = sb + (uint32_t)L.pq;
+    const uint32_t a_ebuf = sb + (uint32_t)L.ebuf, a_red = sb + (uint32_t)L.red, a_mbar = sb + (uint32_t)L.mbar;
+    const uint32_t a_xbuf = sb + (uint32_t)L.xbuf;
+    const uint32_t UB = (uint32_t)fbx_a16(L.ubytes), XOFF = (uint32_t)Kint * S * 4;
+    const uint32_t DC4 = (uint32_t)P.Dc_max * 4;                 // one sequence's emission segment
+    const uint32_t EB = (uint32_t)fbx_a16((size_t)S * DC4);      // one emission buffer
+    const float L2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
+    // u buffer `buf`: rows [Kint][S], then extras slots [C][S][kCX] (max, zm, zs, −)
+    auto a_u = [&](int buf) { return a_u0 + (uint32_t)(buf & 1) * UB; };
+    auto a_x = [&](int buf, int part, int s) { return a_u(buf) + XOFF + (uint32_t)((part * S + s) * kCX) * 4; };
+
+    // ---- the cluster's sequences
+    int bs[S], Ns[S], stt[S];
+    int Tmax = 0;
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int b = grp * S + s;
+        bs[s] = b;
+        Ns[s] = 0;
+        stt[s] = 0;
+        if (b < a.B) {
+            const int N = a.lengths[b];
+            int st = 0;
+            if (BWD) {
+                st = a.status[b];
+                if (a.status2) st |= a.status2[b];
+            }
+            if (N < 1 || N > N_max) st |= FB_SEQ_BAD_LENGTH;
+            const bool skip = (st & FB_SEQ_BAD_LENGTH) || (BWD && st != 0);
+            stt[s] = st;
+            Ns[s] = skip ? 0 : N;
+            Tmax = max(Tmax, Ns[s]);
+        }
+    }
+    // part's pdf range and its emission segment [e_lo, e_lo + e_len)
+    const int d_lo = P.pdf_lo[cr], d_hi = P.pdf_lo[cr + 1];
+    const bool e16 = a.tma != 0;  // 16-byte emission copies (D % 4 == 0, aligned φ)
+    const int e_lo = e16 ? (d_lo & ~3) : d_lo;
+    const int e_len = (e16 ? min(D, (d_hi + 3) & ~3) : d_hi) - e_lo;
+
+    // ---- padded / skipped frames: −∞ lattice rows, zero posterior rows (own states / own pdf range)
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int b = bs[s];
+        if (b >= a.B) continue;
+        const bool lattice = !(stt[s] & FB_SEQ_BAD_LENGTH);
+        for (int n = Ns[s]; n < N_max; ++n) {
+            const size_t rowb = ((size_t)b * N_max + n);
+            for (int j = tid; j < Kc; j += T) {
+                const int o = P.perm[k0 + j];
+                if (o < 0) continue;
+                if (lattice && a.lat) a.lat[rowb * K + o] = NEG_INF;
+                if (want_post && a.post_kind == POST_STATE) a.post[rowb * K + o] = 0.f;
+            }
+            if (pdf_post)
+                for (int d = d_lo + tid; d < d_hi; d += T) a.post[rowb * D + d] = 0.f;
+            if (lattice && a.scale && cr == 0 && tid == 0) a.scale[rowb] = 0.0;
+        }
+    }
+    if (Tmax == 0) {  // nothing to run in this cluster (identical decision in every CTA)
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (cr == 0 && tid == s && bs[s] < a.B) {
+                if (a.logZ) a.logZ[bs[s]] = -INFINITY;
+                a.status[bs[s]] = stt[s];
+            }
+        return;
+    }
+    auto frame = [&](int s, int t) { return BWD ? Ns[s] - 1 - t : t; };
+
+    // ---- schedule and pdf map → shared memory; mbarriers
+    {
+        const uint4 *src = (const uint4 *)(SC.rec + SC.rec_off[cr]);
+        uint4 *dst = (uint4 *)(smem_raw + L.rec);
+        const int n16 = SC.rec_bytes[cr] >> 4;
+        for (int x = tid; x < n16; x += T) dst[x] = src[x];
+    }
+    if (pdf_post)
+        for (int d = d_lo + tid; d < d_hi; d += T) sts_i(a_pq + 4u * (uint32_t)(d - d_lo), (int)P.pq[d]);
+    if (tid == 0) {
+        mbar_init(a_mbar, 1);
+        mbar_init(a_mbar + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // bytes one frame brings from the other parts
+    const uint32_t rx_bytes = (uint32_t)(Kint - Kc) * S * 4 + (uint32_t)(C - 1) * S * kCX * 4;
+
+    // ---- emission segments of step t → ebuf[t & 1] (cp.async, one commit group per step)
+    auto emis_issue = [&](int t) {
+        if (t < Tmax) {
+            const uint32_t base = a_ebuf + (uint32_t)(t & 1) * EB;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (t >= Ns[s]) continue;
+                const float *src = a.emis + ((size_t)bs[s] * N_max + frame(s, t)) * D + e_lo;
+                const uint32_t dst = base + (uint32_t)s * DC4;
+                if (e16) {
+                    for (int x = tid; 4 * x < e_len; x += T) cpa16(dst + 16u * (uint32_t)x, src + 4 * x);
+                } else {
+                    for (int x = tid; x < e_len; x += T) cpa4(dst + 4u * (uint32_t)x, src + x);
+                }
+            }
+        }
+        cpa_commit();
+    };
+    emis_issue(0);
+    emis_issue(1);
+
+    // ---- owned states j = tid + k·T (< Kc); padding / out-of-part slots read a
+    // real emission of the part and are never viable (distance INT_MAX)
+    int pdfk[SPT], distk[SPT], origk[SPT];
+    const int pdf_first = P.ipdf[k0] - e_lo;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+        const int j = tid + k * T;
+        pdfk[k] = pdf_first * 4;
+        distk[k] = INT_MAX;
+        origk[k] = -1;
+        if (j < Kc) {
+            const int i = k0 + j;
+            origk[k] = P.perm[i];
+            if (origk[k] >= 0) {
+                pdfk[k] = (P.ipdf[i] - e_lo) * 4;
+                distk[k] = BWD ? P.idist_start[i] : P.idist_fin[i];
+                if (!(BWD ? G.mask_bwd : G.mask_fwd)) distk[k] = 0;
+            }
+        }
+    }
+    float ar[SPT][S];  // α̂ of the frame being produced (backward posteriors), natural log
+    auto load_alpha = [&](int t) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const bool act = t < Ns[s];
+            const float *ro = a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * K : 0);
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + origk[k]) : NEG_INF;
+        }
+    };
+    // x = α̂·log2e + β̂ of the frame whose posterior is pending: xbuf[j][s] (shared memory)
+    double scale[S];   // C_n / D_n (log2) — identical in every CTA of the cluster
+    float vsum[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) { scale[s] = 0.0; vsum[s] = 0.f; }
+    // termination pairs are reduced per warp at each sequence's last frame: red fields 3, 4
+    for (int x = tid; x < W * S; x += T) {
+        sts_v(a_red + (uint32_t)(x * kCX + 3) * 4, NEG_INF);
+        sts_v(a_red + (uint32_t)(x * kCX + 4) * 4, 0.f);
+    }
+
+    // Store frame t's values h (α̂/β̂, log2) and u of the owned rows; per-warp
+    // reductions (max u, posterior pair) into red[warp][s]; termination pair.
+    auto emit = [&](int t, float (&h)[SPT][S], float (&u)[SPT][S]) {
+        const uint32_t ub = a_u(t);
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            const int j = tid + k * T;
+            if (j < Kc) {
+                float pv[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) pv[s] = ex2(u[k][s]);
+                VS<S>::st(ub + (uint32_t)((k0 + j) * S) * 4, u[k]);
+                VS<S>::st(a_p + (uint32_t)((k0 + j) * S) * 4, pv);
+            }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (t >= Ns[s]) continue;  // CTA-uniform
+            if (a.lat) {
+                float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * K;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k)
+                    if (origk[k] >= 0) latn[origk[k]] = h[k][s] * LN2;
+            }
+            float mx = u[0][s];
+#pragma unroll
+            for (int k = 1; k < SPT; ++k) mx = fmaxf(mx, u[k][s]);
+            mx = warp_max_fast(mx);
+            if (lane == 0) sts_v(a_red + (uint32_t)((warp * S + s) * kCX) * 4, mx);
+            if (want_post) {
+                float x[SPT];
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) {
+                    x[k] = fmaf(ar[k][s], L2E, h[k][s]);
+                    if (tid + k * T < Kc) sts_v(a_xbuf + (uint32_t)((tid + k * T) * S + s) * 4, x[k]);
+                }
+                float zm, zs;
+                warp_lse_vals<float, SPT>(x, zm, zs);
+                if (lane == 0) {
+                    sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 1) * 4, zm);
+                    sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 2) * 4, zs);
+                }
+            }
+            if (t == Ns[s] - 1) {  // termination pair (fwd: u ⊗ ω; bwd: π ⊗ u) — once per sequence
+                float tm = NEG_INF, ts = 0.f;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) {
+                    const int j = tid + k * T;
+                    if (j < Kc && origk[k] >= 0) {
+                        const float w = BWD ? P.iinit2[k0 + j] : P.ifinal2[k0 + j];
+                        lse_push<float>(tm, ts, u[k][s] + w);
+                    }
+                }
+                warp_lse(tm, ts);
+                if (lane == 0) {
+                    sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 3) * 4, tm);
+                    sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 4) * 4, ts);
+                }
+            }
+        }
+    };
+    // warp 0: per-warp reductions → this part's extras slot of buffer t; lane 0 ships the frame
+    auto send = [&](int t) {
+        if (warp != 0) return;
+        if (lane < S) {
+            const int s = lane;
+            float mx = NEG_INF, zm = NEG_INF, zs = 0.f;
+            for (int w = 0; w < W; ++w) {
+                const uint32_t r = a_red + (uint32_t)((w * S + s) * kCX) * 4;
+                mx = fmaxf(mx, lds_v(r, 0.f));
+                if (want_post) lse2(zm, zs, lds_v(r + 4, 0.f), lds_v(r + 8, 0.f));
+            }
+            const uint32_t x = a_x(t, cr, s);
+            sts_v(x, mx);
+            sts_v(x + 4, zm);
+            sts_v(x + 8, zs);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            if (t + 1 < Tmax) mbar_arrive_tx(a_mbar + 8u * (uint32_t)((t + 1) & 1), rx_bytes);
+            const uint32_t rows = a_u(t) + (uint32_t)(k0 * S) * 4, xs = a_x(t, cr, 0);
+            const uint32_t mb = a_mbar + 8u * (uint32_t)(t & 1);
+            for (int q = 0; q < C; ++q) {
+                if (q == cr) continue;
+                bulk_s2s(cl_map(rows, q), rows, (uint32_t)Kc * S * 4, cl_map(mb, q));
+                bulk_s2s(cl_map(xs, q), xs, (uint32_t)S * kCX * 4, cl_map(mb, q));
+            }
+        }
+    };
+
+    // ---- frame 0: π ⊗ v_0 (fwd, L6) / β̂_{N−1} = ω (bwd, L7), exact cluster-wide max
+    if (want_post) load_alpha(0);
+    cpa_wait1();
+    __syncthreads();  // schedule, pq, mbarrier init, step-0 emissions
+    cl_sync();        // every CTA's mbarriers initialised
+    if (tid == 0) mbar_arrive_tx(a_mbar, rx_bytes);
+    float h[SPT][S], u[SPT][S];
+    {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const bool act = 0 < Ns[s];
+            const int lim = act ? (BWD ? frame(s, 0) : Ns[s] - 1) : -1;
+            float mx = NEG_INF;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                const int j = tid + k * T;
+                const bool ok = distk[k] <= lim;
+                const float v = lds_v(a_ebuf + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
+                if (act) vsum[s] += v;
+                const float v2 = v * L2E;
+                const int jj = min(j, Kc - 1);
+                if (!BWD) {
+                    h[k][s] = ok ? P.iinit2[k0 + jj] + v2 : NEG_INF;
+                    u[k][s] = h[k][s];
+                } else {
+                    h[k][s] = ok ? P.ifinal2[k0 + jj] : NEG_INF;
+                    u[k][s] = ok ? h[k][s] + v2 : NEG_INF;
+                }
+                mx = fmaxf(mx, u[k][s]);
+            }
+            mx = warp_max_fast(mx);
+            if (lane == 0) sts_v(a_red + (uint32_t)((warp * S + s) * kCX) * 4, mx);
+        }
+        __syncthreads();
+        const uint32_t init_slot = a_red + (uint32_t)(W * S * kCX) * 4;
+        if (warp == 0 && lane < S) {
+            float mx = NEG_INF;
+            for (int w = 0; w < W; ++w) mx = fmaxf(mx, lds_v(a_red + (uint32_t)((w * S + lane) * kCX) * 4, 0.f));
+            sts_v(init_slot + 4u * (uint32_t)lane, mx);
+        }
+        cl_sync();  // every part's frame-0 maximum visible cluster-wide
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            float c = NEG_INF;
+            for (int q = 0; q < C; ++q) c = fmaxf(c, cl_ldf(cl_map(init_slot + 4u * (uint32_t)s, q)));
+            if (c == NEG_INF) c = 0.f;
+            if (0 < Ns[s]) scale[s] = (double)c;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) { h[k][s] -= c; u[k][s] -= c; }
+            if (cr == 0 && tid == 0 && a.scale && 0 < Ns[s])
+                a.scale[(size_t)bs[s] * N_max + frame(s, 0)] = scale[s] * kLN2;
+        }
+        emit(0, h, u);
+        fence_async_smem();
+        __syncthreads();
+        send(0);
+    }
+
+    // ---- frames 1 … Tmax−1 (+ one flush step t = Tmax for the last posterior rows)
+    const int nsl = SC.warp_nsl[cr * W + warp];
+    const uint32_t mysl = a_rec + (uint32_t)SC.warp_off[cr * W + warp];
+    const int own0 = k0 * S, own1 = (k0 + Kc) * S;  // this part's element range of u / p
+    for (int t = 1; t <= Tmax; ++t) {
+        const bool last = t == Tmax;
+        if (!last) {
+            if (want_post) load_alpha(t);
+            emis_issue(t + 1);
+        }
+        mbar_wait(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
+        const uint32_t up = a_u(t - 1);
+        if (!last) {  // p = 2^u of the other parts' rows
+            for (int e = 4 * tid; e < Kint * S; e += 4 * T) {
+                if (e >= own0 && e < own1) continue;
+                float v[4];
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                             : "r"(up + 4u * (uint32_t)e));
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a_p + 4u * (uint32_t)e), "f"(ex2(v[0])),
+                             "f"(ex2(v[1])), "f"(ex2(v[2])), "f"(ex2(v[3])));
+            }
+        }
+        __syncthreads();  // p complete; this part's extras slot of frame t−1 visible
+        // cluster-wide extras of frame t−1 (fixed part order)
+        float cmax[S], Z[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            float mx = NEG_INF, zm = NEG_INF, zs = 0.f;
+            for (int q = 0; q < C; ++q) {
+                const uint32_t x = a_x(t - 1, q, s);
+                mx = fmaxf(mx, lds_v(x, 0.f));
+                if (want_post) lse2(zm, zs, lds_v(x + 4, 0.f), lds_v(x + 8, 0.f));
+            }
+            cmax[s] = mx;
+            Z[s] = (zm == NEG_INF) ? NEG_INF : zm + lg2(zs);
+        }
+        // posteriors of frame t−1 (Eq. (15), normalised by Z_{t−1} = LSE_k(α̂ + β̂))
+        if (want_post) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (t - 1 >= Ns[s]) continue;
+                const float Zs = (Z[s] == NEG_INF) ? 0.f : Z[s];
+                if (a.post_kind == POST_STATE) {
+                    float *prow = a.post + ((size_t)bs[s] * N_max + frame(s, t - 1)) * K;
+#pragma unroll
+                    for (int k = 0; k < SPT; ++k)
+                        if (origk[k] >= 0)  // implies tid + k·T < Kc
+                            prow[origk[k]] = (Z[s] == NEG_INF)
+                                                 ? 0.f
+                                                 : ex2(lds_v(a_xbuf + (uint32_t)((tid + k * T) * S + s) * 4, 0.f) - Zs);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < SPT; ++k) {
+                        const int j = tid + k * T;
+                        if (j < Kc)
+                            sts_v(a_gbuf + (uint32_t)(j * S + s) * 4,
+                                  (Z[s] == NEG_INF || origk[k] < 0)
+                                      ? 0.f
+                                      : ex2(lds_v(a_xbuf + (uint32_t)(j * S + s) * 4, 0.f) - Zs));
+                    }
+                }
+            }
+        }
+        if (!last) phase_a_vec<S>(mysl, nsl, lane, a_p, a_part);
+        cpa_wait1();
+        __syncthreads();  // part rows, γ rows, step-t emissions complete
+        // pdf-level rows of frame t−1 for this part's pdf range (ascending states, ledger L9)
+        if (pdf_post) {
+            const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (t - 1 >= Ns[s]) continue;
+                float *row = a.post + ((size_t)bs[s] * N_max + frame(s, t - 1)) * D;
+                for (int d = d_lo + tid; d < d_hi; d += T) {
+                    const uint32_t w = lds_u32(a_pq + 4u * (uint32_t)(d - d_lo));
+                    const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
+                    float acc = 0.f;
+                    for (uint32_t i = 0; i < c; ++i) acc += lds_v(a_gbuf + (uint32_t)((q0 + i) * S + s) * 4, 0.f);
+                    row[d] = sgn * acc;
+                }
+            }
+        }
+        if (last) break;
+        // ---- phase B of frame t: y = log2 Σ, emission, lagged normaliser, mask
+        const uint32_t eb = a_ebuf + (uint32_t)(t & 1) * EB;
+        float c[S];
+        int lim[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const bool act = t < Ns[s];
+            c[s] = (cmax[s] == NEG_INF) ? 0.f : cmax[s];  // no viable state: keep 0̄ everywhere
+            lim[s] = act ? (BWD ? frame(s, t) : Ns[s] - 1 - t) : -1;
+            if (act) {
+                scale[s] += (double)c[s];
+                if (cr == 0 && tid == 0 && a.scale) a.scale[(size_t)bs[s] * N_max + frame(s, t)] = scale[s] * kLN2;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            const int j = tid + k * T;
+            float acc[S];
+            VS<S>::ld(a_part + (uint32_t)(min(j, Kc - 1) * S) * 4, acc);
+            bool bad = false;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const float v = lds_v(eb + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
+                vsum[s] += lim[s] >= 0 ? v : 0.f;  // inactive sequences' buffers are stale
+                const bool ok = distk[k] <= lim[s];
+                bad |= ok && !(acc[s] >= kTiny && acc[s] <= kHuge);
+                const float y = lg2(acc[s]);
+                if (!BWD) {
+                    h[k][s] = ok ? y + fmaf(v, L2E, -c[s]) : NEG_INF;
+                    u[k][s] = h[k][s];
+                } else {
+                    h[k][s] = ok ? y - c[s] : NEG_INF;
+                    u[k][s] = ok ? fmaf(v, L2E, h[k][s]) : NEG_INF;
+                }
+            }
+            if (bad) {  // exact max-then-sum rows (rare)
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (!(distk[k] <= lim[s]) || (acc[s] >= kTiny && acc[s] <= kHuge)) continue;
+                    const float y = exact_row_c<S>(BWD ? P.bptr : P.fptr, BWD ? P.bsrc : P.fsrc, BWD ? P.bw2 : P.fw2,
+                                                   k0 + j, s, up);
+                    const float v = lds_v(eb + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
+                    if (!BWD) {
+                        h[k][s] = y + fmaf(v, L2E, -c[s]);
+                        u[k][s] = h[k][s];
+                    } else {
+                        h[k][s] = y - c[s];
+                        u[k][s] = fmaf(v, L2E, h[k][s]);
+                    }
+                }
+            }
+        }
+        emit(t, h, u);
+        fence_async_smem();
+        __syncthreads();  // u / p rows and reductions of frame t complete
+        send(t);
+    }
+
+    // ---- termination: logZ = C + ⊕_k α̂ ⊗ ω (fwd) / logZ_β = D + ⊕_k π ⊗ β̂_0 ⊗ v_0 (bwd);
+    // non-finite emissions flag; both combined over the cluster in fixed order
+    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const float vs = warp_sum(vsum[s]);
+        if (lane == 0) sts_v(a_red + (uint32_t)((warp * S + s) * kCX) * 4 + 20, vs);
+    }
+    __syncthreads();
+    const uint32_t fin = a_red + (uint32_t)((W + 1) * S * kCX) * 4;  // after the frame-0 slot
+    if (warp == 0 && lane < S) {
+        float m = NEG_INF, q = 0.f, vs = 0.f;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t r = a_red + (uint32_t)((w * S + lane) * kCX) * 4;
+            lse2(m, q, lds_v(r + 12, 0.f), lds_v(r + 16, 0.f));
+            vs += lds_v(r + 20, 0.f);
+        }
+        sts_v(fin + 16u * (uint32_t)lane, m);
+        sts_v(fin + 16u * (uint32_t)lane + 4, q);
+        sts_v(fin + 16u * (uint32_t)lane + 8, vs);
+    }
+    cl_sync();
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        if (!(cr == 0 && tid == 0 && bs[s] < a.B)) continue;
+        // float64 combine of the parts' (max, sum) pairs in part order
+        double M = -INFINITY, vq = 0.0;
+        for (int q = 0; q < C; ++q) {
+            const float mq = cl_ldf(cl_map(fin + 16u * (uint32_t)s, q));
+            vq += (double)cl_ldf(cl_map(fin + 16u * (uint32_t)s + 8, q));
+            if (mq != NEG_INF) M = fmax(M, (double)mq);
+        }
+        double tot = 0.0;
+        for (int q = 0; q < C; ++q) {
+            const float mq = cl_ldf(cl_map(fin + 16u * (uint32_t)s, q));
+            if (mq != NEG_INF) tot += (double)cl_ldf(cl_map(fin + 16u * (uint32_t)s + 4, q)) * exp2((double)mq - M);
+        }
+        int st = stt[s];
+        double z = -INFINITY;
+        if (Ns[s] > 0) {
+            z = (M == -INFINITY) ? -INFINITY : (scale[s] + M + log2(tot)) * kLN2;
+            if (!(vq < INFINITY)) st |= FB_SEQ_NONFINITE_INPUT;
+            if (!(z > -INFINITY)) st |= FB_SEQ_EMPTY_LATTICE;
+        }
+        if (st) z = -INFINITY;
+        if (a.logZ) a.logZ[bs[s]] = z;
+        a.status[bs[s]] = st;
+    }
+    cl_sync();  // peers' shared memory stays alive until every remote read is done
+}
+
+using KFn = void (*)(FBArgs);
+// T = 1024 threads (SPT ≤ 4, ≤ 64 registers) or 512 (SPT ≤ 8, ≤ 128 registers)
+template <bool BWD, int S>
+KFn pick_fbc(int spt, int T) {
+    if (T == 1024) {
+        switch (spt) {
+            case 1: return k_fbc<BWD, S, 1, 1024>;
+            case 2: return k_fbc<BWD, S, 2, 1024>;
+            case 3: return k_fbc<BWD, S, 3, 1024>;
+            default: return k_fbc<BWD, S, 4, 1024>;
+        }
+    }
+    switch (spt) {
+        case 1: return k_fbc<BWD, S, 1, 512>;
+        case 2: return k_fbc<BWD, S, 2, 512>;
+        case 3: return k_fbc<BWD, S, 3, 512>;
+        case 4: return k_fbc<BWD, S, 4, 512>;
+        case 6: return k_fbc<BWD, S, 6, 512>;
+        default: return k_fbc<BWD, S, 8, 512>;
+    }
+}
+template KFn pick_fbc<(bool)FBX_BWD, FBX_S>(int, int);
+
+}  // namespace fbx

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -54,7 +55,10 @@ struct RowLists {
 // esize = bytes per element of the gathered u / p arrays; index words hold byte
 // offsets relative to the gathered array and are rebased to shared-memory
 // offsets by the caller once the layout is known.
-bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, int Lmax, HostSched &hs) {
+// vec: gathered elements are S-float vectors of the cluster kernel (esize = 4·S);
+// slots are then placed by local search under the per-phase bank model only.
+bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, int Lmax, HostSched &hs,
+                        bool vec = false) {
     const int W = T / 32;
     struct RowG { int row, len; };
     std::vector<RowG> cls[6];  // g = 1, 2, 4, 8, 16, 32
@@ -112,7 +116,10 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     const float padw = (mode == MODE_FACTORED) ? 0.0f : -INFINITY;
     // shared-memory bank of a gathered element (32 banks of 4 bytes; an 8-byte
     // element is treated as one of 16 double-width banks)
-    const int nbanks = esize == 4 ? 32 : 16;
+    const int nbanks = esize == 4 ? 32 : (vec ? 128 / esize : 16);
+    // a warp request of esize-byte elements is served in esize/4 phases of
+    // 32/(esize/4) lanes (vec); each phase costs its most-loaded bank
+    const int nphase = vec ? esize / 4 : 1, lpp = 32 / nphase;
     auto bank_of = [&](uint32_t boff) { return (int)((boff / (uint32_t)esize) % (uint32_t)nbanks); };
     std::vector<std::vector<long long>> rem(32);
     for (int w = 0; w < W; ++w) {
@@ -149,7 +156,10 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
             const int Ls = s.L;
             std::vector<long long> grid((size_t)Ls * 32, -1);  // arc index or -1 (null)
             auto addr_of = [&](long long arc) { return (uint32_t)rl.other[arc] * (uint32_t)esize; };
-            {
+            if (vec) {
+                for (int l = 0; l < 32; ++l)
+                    for (size_t c0 = 0; c0 < rem[l].size(); ++c0) grid[c0 * 32 + l] = rem[l][c0];
+            } else {
                 // grid[c*32 + l] = arc of lane l in colour (slot) c; bank_c[b*Ls + c] =
                 // lane whose arc of bank b has colour c (proper edges only)
                 std::vector<int> bank_c((size_t)nbanks * Ls, -1);
@@ -221,20 +231,24 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
             // the two arc-rows' summed wavefront count does not grow (seeded, so the
             // schedule is deterministic)
             auto row_cost = [&](int r) {
-                uint32_t seen[32];
-                int ns = 0, cnt[32] = {0}, worst = 1;
-                for (int l = 0; l < 32; ++l) {
-                    const long long arc = grid[(size_t)r * 32 + l];
-                    if (arc < 0) continue;
-                    const uint32_t ad = addr_of(arc);
-                    bool dup = false;
-                    for (int x = 0; x < ns; ++x)
-                        if (seen[x] == ad) { dup = true; break; }
-                    if (dup) continue;
-                    seen[ns++] = ad;
-                    worst = std::max(worst, ++cnt[bank_of(ad)]);
+                int total = 0;
+                for (int ph = 0; ph < nphase; ++ph) {
+                    uint32_t seen[32];
+                    int ns = 0, cnt[32] = {0}, worst = 1;
+                    for (int l = ph * lpp; l < (ph + 1) * lpp; ++l) {
+                        const long long arc = grid[(size_t)r * 32 + l];
+                        if (arc < 0) continue;
+                        const uint32_t ad = addr_of(arc);
+                        bool dup = false;
+                        for (int x = 0; x < ns; ++x)
+                            if (seen[x] == ad) { dup = true; break; }
+                        if (dup) continue;
+                        seen[ns++] = ad;
+                        worst = std::max(worst, ++cnt[bank_of(ad)]);
+                    }
+                    total += worst;
                 }
-                return worst;
+                return total;
             };
             if (Ls > 1 && mode == MODE_FACTORED) {
                 std::vector<int> rc(Ls);
@@ -305,6 +319,143 @@ struct Packer {
 };
 
 bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
+
+// Host image of a CPlan (fb_internal.h).
+struct HostCPlan {
+    int C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0, emis16 = 0;
+    std::vector<int> part_off, pdf_lo, perm, ipdf, idf, ids;
+    std::vector<float> ii2, if2;
+    std::vector<unsigned> pq;
+    HostSched hf, hb;
+    std::vector<int> fptr, fsrc, bptr, bsrc;
+    std::vector<float> fw2, bw2;
+    size_t smem_fwd = 0, smem_bwd = 0;
+};
+
+// Cluster plan for one shared graph (G == 1, factored mode): C parts along
+// ascending pdf ranges balanced on arcs (both directions) + a per-state phase-B
+// cost, internal order (pdf, state id) inside a part, each part padded to a
+// multiple of 4 states; per-part sliced-ELL schedules over S-float elements.
+bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, const std::vector<int> &pdf,
+                        const std::vector<int> &dist_fin, const std::vector<int> &dist_start,
+                        const std::vector<float> &init2, const std::vector<float> &final2, int C, int S, int Lmax,
+                        HostCPlan &cp, int Tforce = 0) {
+    // 1024 threads (≤ 4 owned states each) unless the part needs more states per thread
+    int T = 1024;
+    if (const char *e = std::getenv("FBX_CLUSTER_T")) T = std::atoi(e) == 512 ? 512 : 1024;
+    if (Tforce) T = Tforce;
+    const int W = T / 32;
+    cp = HostCPlan();
+    cp.C = C; cp.S = S; cp.T = T;
+    std::vector<double> cost(D, 0.0);
+    for (int k = 0; k < K; ++k)
+        cost[pdf[k]] += (in.ptr[k + 1] - in.ptr[k]) + (out.ptr[k + 1] - out.ptr[k]) + 8.0;
+    double total = 0;
+    for (double x : cost) total += x;
+    cp.pdf_lo.assign(C + 1, 0);
+    cp.pdf_lo[C] = D;
+    {
+        double acc = 0;
+        int c = 1;
+        for (int d = 0; d < D && c < C; ++d) {
+            acc += cost[d];
+            while (c < C && acc >= total * c / C) cp.pdf_lo[c++] = d + 1;
+        }
+        for (; c < C; ++c) cp.pdf_lo[c] = D;
+    }
+    std::vector<std::pair<int, int>> ps;
+    for (int k = 0; k < K; ++k) ps.push_back({pdf[k], k});
+    std::sort(ps.begin(), ps.end());
+    cp.part_off.assign(C + 1, 0);
+    std::vector<int> inv(K, -1);
+    {
+        size_t x = 0;
+        for (int c = 0; c < C; ++c) {
+            const int start = (int)cp.perm.size();
+            while (x < ps.size() && ps[x].first < cp.pdf_lo[c + 1]) {
+                inv[ps[x].second] = (int)cp.perm.size();
+                cp.perm.push_back(ps[x].second);
+                ++x;
+            }
+            if ((int)cp.perm.size() == start) return false;  // an empty part
+            while (cp.perm.size() % 4) cp.perm.push_back(-1);
+            cp.part_off[c + 1] = (int)cp.perm.size();
+            cp.Kc_max = std::max(cp.Kc_max, cp.part_off[c + 1] - start);
+        }
+    }
+    cp.K_int = (int)cp.perm.size();
+    if ((long long)cp.K_int * S * 4 > 65536) return false;  // 16-bit gather offsets
+    cp.spt = (cp.Kc_max + T - 1) / T;
+    if (T == 1024 && cp.spt > 4)
+        return build_cluster_plan(in, out, K, D, pdf, dist_fin, dist_start, init2, final2, C, S, Lmax, cp, 512);
+    if (cp.spt > 8) return false;
+    cp.spt = cp.spt <= 4 ? cp.spt : (cp.spt <= 6 ? 6 : 8);
+    const int Ki = cp.K_int;
+    cp.ipdf.assign(Ki, 0); cp.idf.assign(Ki, kFar); cp.ids.assign(Ki, kFar);
+    cp.ii2.assign(Ki, -INFINITY); cp.if2.assign(Ki, -INFINITY);
+    for (int i = 0; i < Ki; ++i) {
+        const int o = cp.perm[i];
+        if (o < 0) continue;
+        cp.ipdf[i] = pdf[o]; cp.idf[i] = dist_fin[o]; cp.ids[i] = dist_start[o];
+        cp.ii2[i] = init2[o]; cp.if2[i] = final2[o];
+    }
+    // pdf → (first local position, count) inside its part
+    cp.pq.assign(D, 0u);
+    for (int c = 0; c < C; ++c)
+        for (int i = cp.part_off[c]; i < cp.part_off[c + 1]; ++i) {
+            const int o = cp.perm[i];
+            if (o < 0) continue;
+            unsigned &w = cp.pq[pdf[o]];
+            if ((w >> 16) == 0) w = (unsigned)(i - cp.part_off[c]);
+            w += 1u << 16;
+        }
+    // emission segment of each part
+    cp.emis16 = (D % 4) == 0;
+    int dmax = 0;
+    for (int c = 0; c < C; ++c) {
+        int lo = cp.pdf_lo[c], hi = cp.pdf_lo[c + 1];
+        if (cp.emis16) { lo &= ~3; hi = std::min(D, (hi + 3) & ~3); }
+        dmax = std::max(dmax, hi - lo);
+    }
+    cp.Dc_max = std::max(4, (dmax + 3) & ~3);
+    // per-part schedules and the exact-fallback arc lists (internal ids)
+    auto lists = [&](const RowLists &rl, std::vector<int> &ptr, std::vector<int> &src, std::vector<float> &w2) {
+        ptr.assign(Ki + 1, 0);
+        for (int i = 0; i < Ki; ++i) {
+            const int o = cp.perm[i];
+            if (o >= 0)
+                for (int a = rl.ptr[o]; a < rl.ptr[o + 1]; ++a) {
+                    src.push_back(inv[rl.other[a]]);
+                    w2.push_back((float)(rl.w[a] * kLog2e));
+                }
+            ptr[i + 1] = (int)src.size();
+        }
+    };
+    lists(in, cp.fptr, cp.fsrc, cp.fw2);
+    lists(out, cp.bptr, cp.bsrc, cp.bw2);
+    for (int dir = 0; dir < 2; ++dir) {
+        const RowLists &rl = dir ? out : in;
+        HostSched &hs = dir ? cp.hb : cp.hf;
+        for (int c = 0; c < C; ++c) {
+            RowLists pl;
+            const int Kc = cp.part_off[c + 1] - cp.part_off[c];
+            pl.ptr.assign(Kc + 1, 0);
+            for (int r = 0; r < Kc; ++r) {
+                const int o = cp.perm[cp.part_off[c] + r];
+                if (o >= 0)
+                    for (int a = rl.ptr[o]; a < rl.ptr[o + 1]; ++a) {
+                        pl.other.push_back(inv[rl.other[a]]);
+                        pl.w.push_back(rl.w[a]);
+                    }
+                pl.ptr[r + 1] = (int)pl.other.size();
+            }
+            if (!build_member_sched(pl, Kc, T, MODE_FACTORED, 4 * S, Lmax, hs, true)) return false;
+        }
+    }
+    cp.smem_fwd = cl_layout(cp.hf.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, false).total;
+    cp.smem_bwd = cl_layout(cp.hb.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, true).total;
+    return cp.smem_fwd <= (size_t)kSmemLimit && cp.smem_bwd <= (size_t)kSmemLimit;
+}
 
 }  // namespace
 
@@ -416,6 +567,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         init2[i] = (float)((double)log_init[i] * kLog2e);
         final2[i] = (float)((double)log_final[i] * kLog2e);
     }
+    RowLists in0, out0;  // member 0's arc lists (cluster plan of a shared graph)
     for (int g = 0; g < G; ++g) {
         const int s0 = state_offsets[g], K = state_offsets[g + 1] - s0;
         RowLists in, outl;
@@ -489,6 +641,35 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         slot_sptr.push_back((int)slot_states.size());
         slot_off[g + 1] = slot_off[g] + local;
         gr.pm.U_max = std::max(gr.pm.U_max, local);
+        if (G == 1) { in0 = std::move(in); out0 = std::move(outl); }
+    }
+    gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
+    gr.bwd.bytes_max = hb.bytes_max; gr.bwd.slots_max = hb.slots_max;
+    gr.vit.bytes_max = hv.bytes_max; gr.vit.slots_max = hv.slots_max;
+    gr.vit_ok = vit_ok && viterbi_smem_bytes(gr) <= (size_t)kSmemLimit;
+    if (!gr.vit_ok) hv = HostSched();
+    gr.pm.U_tot = slot_off[G];
+    // cluster plan (k_fbc) for a shared factored graph: the first (C, S) that fits
+    // shared memory, C CTAs per cluster, S sequences per cluster
+    HostCPlan hcp;
+    bool cp_ok = false;
+    // one-CTA-per-sequence kernels: schedule, state arrays and i16 pdf maps in shared memory
+    gr.legacy_ok = !(gr.pm.U_max >= 32768 || (long long)D * 2 > 65536 || smem_bytes(gr, false, false) > (size_t)kSmemLimit ||
+                     smem_bytes(gr, true, true) + std::max(pdf_region(POST_GRAD, gr.pm.U_max, D).bytes,
+                                                           pdf_region(POST_PDF_COMPACT, gr.pm.U_max, D).bytes) >
+                         (size_t)kSmemLimit);
+    const bool want_cluster = (flags & FB_GRAPH_CLUSTER) || std::getenv("FBX_CLUSTER") || !gr.legacy_ok;
+    if (G == 1 && gr.mode == MODE_FACTORED && want_cluster) {
+        std::vector<std::pair<int, int>> cand = {{2, 2}, {4, 2}, {8, 2}, {4, 4}, {8, 4}};
+        if (const char *e = std::getenv("FBX_CLUSTER")) {
+            int c = 0, sq = 0;
+            if (std::sscanf(e, "%d,%d", &c, &sq) == 2) cand = {{c, sq}};
+        }
+        for (auto cs : cand) {
+            if (cs.first < 2 || cs.first > 8 || !(cs.second == 2 || cs.second == 4)) continue;
+            if (build_cluster_plan(in0, out0, K_tot, D, pdf, dist_fin, dist_start, init2, final2, cs.first,
+                                   cs.second, 12, hcp)) { cp_ok = true; break; }
+        }
     }
     gr.pm.U_tot = slot_off[G];
     for (int i = 0; i < K_tot; ++i) {
@@ -497,18 +678,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     }
     // index words hold byte offsets relative to the gathered array (p in factored
     // mode, u in exact mode), which the kernel addresses as [offset + base]
-    gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
-    gr.bwd.bytes_max = hb.bytes_max; gr.bwd.slots_max = hb.slots_max;
-    gr.vit.bytes_max = hv.bytes_max; gr.vit.slots_max = hv.slots_max;
-    gr.vit_ok = vit_ok && viterbi_smem_bytes(gr) <= (size_t)kSmemLimit;
-    if (!gr.vit_ok) hv = HostSched();
-    gr.pm.U_tot = slot_off[G];
-    if (gr.pm.U_max >= 32768 || (long long)D * 2 > 65536) return FB_ERR_UNSUPPORTED;  // i16 pdf maps in smem
-    if (smem_bytes(gr, false, false) > (size_t)kSmemLimit ||
-        smem_bytes(gr, true, true) + std::max(pdf_region(POST_GRAD, gr.pm.U_max, D).bytes,
-                                              pdf_region(POST_PDF_COMPACT, gr.pm.U_max, D).bytes) >
-            (size_t)kSmemLimit)
-        return FB_ERR_UNSUPPORTED;
+    if (!gr.legacy_ok && !cp_ok) return FB_ERR_UNSUPPORTED;
 
     // pack and upload
     Packer pk;
@@ -525,6 +695,22 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         return o;
     };
     SO of = put_sched(hf), ob = put_sched(hb), ov = put_sched(hv);
+    SO ocf{}, ocb{};
+    size_t o_cpo = 0, o_cpl = 0, o_cpe = 0, o_cpd = 0, o_cdf = 0, o_cds = 0, o_ci2 = 0, o_cf2 = 0, o_cpq = 0,
+           o_fp = 0, o_fs = 0, o_fw = 0, o_bp = 0, o_bs = 0, o_bw = 0;
+    if (cp_ok) {
+        ocf = put_sched(hcp.hf); ocb = put_sched(hcp.hb);
+        o_cpo = pk.put(hcp.part_off); o_cpl = pk.put(hcp.pdf_lo); o_cpe = pk.put(hcp.perm); o_cpd = pk.put(hcp.ipdf);
+        o_cdf = pk.put(hcp.idf); o_cds = pk.put(hcp.ids); o_ci2 = pk.put(hcp.ii2); o_cf2 = pk.put(hcp.if2);
+        o_cpq = pk.put(hcp.pq);
+        o_fp = pk.put(hcp.fptr); o_fs = pk.put(hcp.fsrc); o_fw = pk.put(hcp.fw2);
+        o_bp = pk.put(hcp.bptr); o_bs = pk.put(hcp.bsrc); o_bw = pk.put(hcp.bw2);
+        CPlan &c = gr.cp;
+        c.ok = 1; c.C = hcp.C; c.S = hcp.S; c.T = hcp.T; c.spt = hcp.spt; c.K_int = hcp.K_int;
+        c.Kc_max = hcp.Kc_max; c.Dc_max = hcp.Dc_max; c.emis16 = hcp.emis16;
+        c.fwd.bytes_max = hcp.hf.bytes_max; c.fwd.slots_max = hcp.hf.slots_max;
+        c.bwd.bytes_max = hcp.hb.bytes_max; c.bwd.slots_max = hcp.hb.slots_max;
+    }
     size_t o_so = pk.put(slot_off), o_spd = pk.put(slot_pdf), o_ssp = pk.put(slot_sptr),
            o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot), o_spo = pk.put(slot_pos);
     if (flags & FB_GRAPH_DRY_RUN) {
@@ -568,6 +754,16 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     set_sched(gr.fwd, of);
     set_sched(gr.bwd, ob);
     set_sched(gr.vit, ov);
+    if (cp_ok) {
+        CPlan &c = gr.cp;
+        set_sched(c.fwd, ocf);
+        set_sched(c.bwd, ocb);
+        c.part_off = (const int *)P(o_cpo); c.pdf_lo = (const int *)P(o_cpl); c.perm = (const int *)P(o_cpe);
+        c.ipdf = (const int *)P(o_cpd); c.idist_fin = (const int *)P(o_cdf); c.idist_start = (const int *)P(o_cds);
+        c.iinit2 = (const float *)P(o_ci2); c.ifinal2 = (const float *)P(o_cf2); c.pq = (const unsigned *)P(o_cpq);
+        c.fptr = (const int *)P(o_fp); c.fsrc = (const int *)P(o_fs); c.fw2 = (const float *)P(o_fw);
+        c.bptr = (const int *)P(o_bp); c.bsrc = (const int *)P(o_bs); c.bw2 = (const float *)P(o_bw);
+    }
     gr.pm.slot_off = (const int *)P(o_so); gr.pm.slot_pdf = (const int *)P(o_spd);
     gr.pm.slot_sptr = (const int *)P(o_ssp); gr.pm.slot_states = (const int *)P(o_sst);
     gr.pm.pdf_slot = (const int *)P(o_pds);
@@ -594,7 +790,8 @@ extern "C" fb_status fb_graph_info(fb_graph h, int64_t *out) {
     const Graph &g = h->g;
     int64_t v[16] = {g.G, g.K_tot, g.nnz, g.D, g.T, g.spt, g.mode,
                      (int64_t)smem_bytes(g, false, false), (int64_t)smem_bytes(g, true, true),
-                     g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max, g.fwd.bytes_max, g.bwd.bytes_max};
+                     g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max,
+                     g.cp.ok ? g.cp.C : 0, g.cp.ok ? g.cp.S : 0};
     std::memcpy(out, v, sizeof v);
     return FB_OK;
 }

@@ -61,6 +61,35 @@ struct PdfMap {
     long long U_tot = 0;
 };
 
+// Cluster plan of a shared (G == 1) factored graph for k_fbc: a thread-block
+// cluster of C CTAs runs S sequences in lockstep.  The K states are split into
+// C parts along ascending pdf ranges (every state of a pdf lives in one part, so
+// pdf-level posterior rows are part-local); part c owns the contiguous
+// internal states [part_off[c], part_off[c+1]) (each part padded to a multiple
+// of 4 with inert states) and computes their rows for all S sequences, reading
+// the gathered vector p = 2^u of every state from its own shared memory.  After
+// each frame a CTA ships its rows of u to the other C−1 CTAs with bulk
+// shared→shared copies (DSMEM) that complete on the receivers' mbarriers.
+// Schedules are the grouped sliced-ELL of Sched with S-float gathered elements
+// (member c = part c's rows); index words are byte offsets into p[K_int][S].
+struct CPlan {
+    int ok = 0, C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0;
+    int emis16 = 0;                     // emission segments are 16-byte aligned (D % 4 == 0)
+    const int *part_off = nullptr;      // [C+1] internal state offsets
+    const int *pdf_lo = nullptr;        // [C+1] part c owns pdfs [pdf_lo[c], pdf_lo[c+1])
+    const int *perm = nullptr;          // [K_int] original state id (−1: padding)
+    const int *ipdf = nullptr;          // [K_int] pdf (0 for padding)
+    const int *idist_fin = nullptr;     // [K_int] as Graph::dist_fin (kFar for padding)
+    const int *idist_start = nullptr;   // [K_int]
+    const float *iinit2 = nullptr;      // [K_int] π·log2(e) (−∞ for padding)
+    const float *ifinal2 = nullptr;     // [K_int] ω·log2(e)
+    const unsigned *pq = nullptr;       // [D] first local position of the pdf's states | count << 16
+    Sched fwd, bwd;                     // member c: part c's rows (in-arcs / out-arcs)
+    // exact fallback rows (internal ids, log2 weights): forward in-arcs, backward out-arcs
+    const int *fptr = nullptr, *fsrc = nullptr, *bptr = nullptr, *bsrc = nullptr;
+    const float *fw2 = nullptr, *bw2 = nullptr;
+};
+
 struct Graph {
     int G = 0, K_tot = 0, D = 0, T = 0, W = 0, spt = 1, mode = 0;
     int mask_fwd = 0, mask_bwd = 0;  // any state ever masked by the viability distances
@@ -80,6 +109,8 @@ struct Graph {
     Sched vit;        // forward (in-arc) schedule with natural-log weights for fb_viterbi
     int vit_ok = 0;   // the Viterbi schedule fits shared memory
     PdfMap pm;
+    CPlan cp;         // cluster plan (k_fbc); cp.ok == 0: one CTA per sequence (k_fb)
+    int legacy_ok = 1; // the one-CTA-per-sequence kernels fit (else only the cluster path runs)
     void *block = nullptr;
     size_t block_bytes = 0;
     bool dry = false;
@@ -131,6 +162,33 @@ FBX_HD inline PdfRegion pdf_region(int kind, int U_max, int D) {
     R.pq = o; if (kind == POST_PDF_DENSE || kind == POST_GRAD) o += fbx_a16((size_t)D * 4);
     R.bytes = (kind == POST_PDF_DENSE || kind == POST_PDF_COMPACT || kind == POST_GRAD) ? o : 0;
     return R;
+}
+
+// Shared-memory carve-up of one k_fbc CTA (host and device agree):
+// rec (part schedule) | u[2] (per buffer: K_int·S floats, then C extras slots of
+// S × 8 floats) | p (K_int·S) | part (Kc_max·S) | gbuf (Kc_max·S, pdf-level
+// posteriors) | pq (Dc_max, pdf-level) | ebuf[2][S][Dc_max] emission segments
+// | red (per warp × seq × 8 floats, + frame-0 and termination slots) | mbar[2].
+constexpr int kCX = 8;  // floats per (part, sequence) extras slot
+struct CLayout {
+    size_t rec, u, ubytes, p, part, gbuf, xbuf, pq, ebuf, red, mbar, total;
+};
+FBX_HD inline CLayout cl_layout(int rec_bytes, int K_int, int Kc_max, int Dc_max, int S, int C, int W, bool pdfpost) {
+    CLayout L;
+    size_t o = 0;
+    L.rec = o; o += fbx_a16((size_t)rec_bytes);
+    L.ubytes = (size_t)K_int * S * 4 + (size_t)C * S * kCX * 4;
+    L.u = o; o += 2 * fbx_a16(L.ubytes);
+    L.p = o; o += fbx_a16((size_t)K_int * S * 4);
+    L.part = o; o += fbx_a16((size_t)Kc_max * S * 4);
+    L.gbuf = o; if (pdfpost) o += fbx_a16((size_t)Kc_max * S * 4);
+    L.xbuf = o; if (pdfpost) o += fbx_a16((size_t)Kc_max * S * 4);
+    L.pq = o; if (pdfpost) o += fbx_a16((size_t)Dc_max * 4);
+    L.ebuf = o; o += 2 * fbx_a16((size_t)S * Dc_max * 4);
+    L.red = o; o += fbx_a16((size_t)(W + 2) * S * kCX * 4);
+    L.mbar = o; o += 16;
+    L.total = o;
+    return L;
 }
 
 // Dynamic shared memory needed by a forward/backward launch over this graph.

@@ -380,9 +380,63 @@ static fb_status check_launch(const char *what) {
     return FB_OK;
 }
 
+template <bool BWD, int S>
+KFn pick_fbc(int spt, int T);
+extern template KFn pick_fbc<false, 2>(int, int);
+extern template KFn pick_fbc<false, 4>(int, int);
+extern template KFn pick_fbc<true, 2>(int, int);
+extern template KFn pick_fbc<true, 4>(int, int);
+
+// Does this launch run the cluster-batched kernel k_fbc (fb_cluster.cu)?
+static bool use_cluster(bool bwd, const FBArgs &a, bool raw) {
+    const Graph &G = a.g;
+    if (!G.cp.ok || raw || G.G != 1 || G.mode != MODE_FACTORED) return false;
+    return !bwd || a.post_kind != POST_PDF_COMPACT;
+}
+
+// CTAs a launch occupies (one per SM): what lfmmi leaves to the numerator pass.
+static int den_ctas(const Graph &G, const FBArgs &a) {
+    if (use_cluster(false, a, false)) return G.cp.C * ((a.B + G.cp.S - 1) / G.cp.S);
+    return a.B;
+}
+
+static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
+    const Graph &G = a.g;
+    const CPlan &P = G.cp;
+    FBArgs aa = a;
+    aa.tma = (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0);  // 16-byte emission copies
+    KFn fn = bwd ? (P.S == 4 ? pick_fbc<true, 4>(P.spt, P.T) : pick_fbc<true, 2>(P.spt, P.T))
+                 : (P.S == 4 ? pick_fbc<false, 4>(P.spt, P.T) : pick_fbc<false, 2>(P.spt, P.T));
+    const size_t sm = cl_layout(bwd ? P.bwd.bytes_max : P.fwd.bytes_max, P.K_int, P.Kc_max, P.Dc_max, P.S, P.C,
+                                P.T / 32, bwd).total;
+    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3((unsigned)(P.C * ((a.B + P.S - 1) / P.S)), 1, 1);
+    cfg.blockDim = dim3((unsigned)P.T, 1, 1);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)P.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    {
+        ProfScope ps(bwd ? "k_fbc_bwd[G=1]" : "k_fbc_fwd[G=1]", s);
+        e = cudaLaunchKernelEx(&cfg, fn, aa);
+    }
+    if (e != cudaSuccess) { set_cuda_error("k_fbc launch", (int)e); return FB_ERR_CUDA; }
+    return check_launch("k_fbc launch");
+}
+
 // idle_sms > 0: launch only as many (persistent) CTAs as fit on that many SMs.
 static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw = false, int idle_sms = 0) {
     const Graph &G = a.g;
+    if (use_cluster(bwd, a, raw)) return launch_fbc(bwd, a, s);
+    if (!G.legacy_ok) return FB_ERR_UNSUPPORTED;
     const bool post_pdf = bwd && a.post_kind != POST_NONE && a.post_kind != POST_STATE;
     size_t sm = smem_bytes(G, bwd, post_pdf) + (post_pdf ? pdf_region(a.post_kind, G.pm.U_max, a.D).bytes : 0);
     // φ rows through TMA when they are 16-byte aligned and the two row buffers fit
@@ -556,7 +610,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     int dev = 0, nsm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    const int idle = nsm - std::min(B, nsm);
+    const int idle = nsm - std::min(den_ctas(den->g, base_args(den, log_emis, lengths, B, N_max)), nsm);
     const int confine = idle >= 8 ? idle : 0;
     {
         FBArgs a = base_args(num, log_emis, lengths, B, N_max);

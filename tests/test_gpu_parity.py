@@ -294,3 +294,73 @@ def test_viterbi_c2_numerators(fbx):
 def test_viterbi_c3_den(fbx):
     w = synth.make_c3(seed=3, B=4, N=80)
     _viterbi_check(fbx, w.den, w.emis, np.array([80, 13, 1, 55], np.int32))
+
+
+# ------------------------------------------------------------------ cluster-batched kernel (k_fbc)
+
+@pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2"])
+def test_cluster_configs_vs_oracle(fbx, cs, monkeypatch):
+    """Every (C CTAs, S sequences) cluster configuration of a shared factored
+    graph against the oracle: logZ (both directions), α̂ + scale, state and pdf
+    posteriors, ragged lengths (a length-1 sequence, an odd batch)."""
+    monkeypatch.setenv("FBX_CLUSTER", cs)
+    w = synth.make_c4(seed=21, B=5, N=48, K=1500, nnz=10000, D=1000, kind="softmax4")
+    lens = np.array([48, 1, 30, 48, 17], np.int32)
+    r = run_fb(fbx, w.den, w.emis, lens)
+    C, S = (int(x) for x in cs.split(","))
+    assert (r["g"].info["cluster_C"], r["g"].info["cluster_S"]) == (C, S)
+    ref = oracle.fb_batch(w.den, w.emis, lens, alpha=True, post=True, post_pdf=True)
+    assert (r["st"] == 0).all()
+    check_logZ(r["logZ"], ref["logZ"], np.ones(5, bool))
+    check_logZ(r["logZb"], ref["logZ"], np.ones(5, bool))
+    K = w.den.K
+    assert np.abs(r["post"].reshape(ref["post"].shape) - ref["post"]).max() <= TOL_POST
+    # α̂ + C_n = α (float64 oracle), on finite entries; −∞ exactly where the oracle has −∞
+    a = r["alpha"].cpu().numpy().reshape(5, 48, K).astype(np.float64) + r["scale"].cpu().numpy()[:, :, None]
+    ra = ref["alpha"].reshape(5, 48, K)
+    for b in range(5):
+        fin = np.isfinite(ra[b, : lens[b]])
+        assert (np.isfinite(a[b, : lens[b]]) == fin).all()
+        d = np.abs(a[b, : lens[b]][fin] - ra[b, : lens[b]][fin]) / np.maximum(1.0, np.abs(ra[b, : lens[b]][fin]))
+        assert d.max() <= 1e-5, d.max()
+    rp = run_fb(fbx, w.den, w.emis, lens, post="pdf")
+    assert np.abs(rp["post"] - ref["post_pdf"]).max() <= TOL_POST
+
+
+def test_cluster_matches_one_cta_per_sequence(fbx):
+    """k_fbc (FB_GRAPH_CLUSTER) and the one-CTA-per-sequence kernel on the same
+    C4-shaped inputs; both within the gates of the oracle."""
+    import torch
+
+    w = synth.make_c4(seed=22, B=4, N=64, L_range=(10, 30))
+    lens = np.array([64, 40, 64, 33], np.int32)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    out = {}
+    for flags in (0, 4):
+        den = fbx.Graph.from_host(w.den, flags)
+        assert (den.info["cluster_C"] > 0) == (flags == 4)
+        loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(w.emis), dev(lens))
+        torch.cuda.synchronize()
+        out[flags] = (loss.cpu().numpy(), grad.cpu().numpy(), st.cpu().numpy())
+    ref = oracle.lfmmi_batch(synth.compose(w.nums), synth.compose([w.den]), w.emis, lens)
+    for flags in (0, 4):
+        loss, grad, st = out[flags]
+        assert (st == 0).all()
+        assert np.abs(grad - ref["grad"]).max() <= TOL_GRAD
+        assert (np.abs(loss - ref["loss"]) / np.maximum(1, np.abs(ref["logZ_den"]))).max() <= TOL_LOGZ
+    assert np.abs(out[0][1] - out[4][1]).max() <= 2 * TOL_GRAD
+
+
+def test_paper_shape_den_n2(fbx):
+    """N2: the paper's Table 1 denominator shape (3022 states, 50,984 arcs, D = 84;
+    P:445-457), whose schedule exceeds one SM's shared memory — it runs split
+    over a cluster.  Reduced B and N; oracle parity on logZ, posteriors, grad rows."""
+    den, emis = synth.make_paper_shape(seed=6, B=3, N=70)
+    lens = np.array([70, 70, 23], np.int32)
+    r = run_fb(fbx, den, emis, lens, post="pdf")
+    assert r["g"].info["cluster_C"] >= 2
+    ref = oracle.fb_batch(den, emis, lens, post=True, post_pdf=True)
+    assert (r["st"] == 0).all()
+    check_logZ(r["logZ"], ref["logZ"], np.ones(3, bool))
+    check_logZ(r["logZb"], ref["logZ"], np.ones(3, bool))
+    assert np.abs(r["post"] - ref["post_pdf"]).max() <= TOL_POST
