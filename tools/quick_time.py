@@ -48,7 +48,8 @@ if "c4" in which:
     t0 = time.time()
     w = synth.make_c4(seed=4)
     print("gen c4", time.time() - t0, flush=True)
-    num = fbx.Graph.from_host(synth.compose(w.nums)); den = fbx.Graph.from_host(w.den)
+    num = fbx.Graph.from_host(synth.compose(w.nums), int(os.environ.get("FBX_NUM_FLAGS", "0")))
+    den = fbx.Graph.from_host(w.den, int(os.environ.get("FBX_DEN_FLAGS", "0")))
     print("num", num.info, "\nden", den.info, flush=True)
     e = torch.from_numpy(w.emis).cuda(); L = torch.from_numpy(w.lengths).cuda()
     grad = torch.empty_like(e)
