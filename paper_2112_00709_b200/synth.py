@@ -399,9 +399,12 @@ def c5_emissions(seed: int, idx: np.ndarray, N_max: int, D: int) -> np.ndarray:
     return out
 
 
-def make_paper_shape(seed: int = 6, B: int = 128, N: int = 700):
-    """Table 1 shape: den 3022 states / 50,984 arcs, num 454 / 1036, D = 84."""
+def make_paper_shape(seed: int = 6, B: int = 128, N: int = 700, L_range=(190, 211)) -> Workload:
+    """N2, the paper's Table 1 shape: den 3022 states / 50,984 arcs with
+    a pdf surjection onto D = 84 outputs; B numerator graphs of ≈454 states / ≈1036
+    arcs (C2 recipe with L ~ U[190, 210] phones, capped at 454 states); all N_b = N."""
     rng = np.random.Generator(np.random.PCG64(seed))
     den = denominator_graph(rng, 3022, 50984, D=84, pdf_mode="surjection")
+    nums = [numerator_graph(rng, int(rng.integers(*L_range)), 84, "random", k_max=454) for _ in range(B)]
     em = emissions(rng, B, N, 84)
-    return den, em
+    return Workload("N2", B, N, 84, np.full(B, N, np.int32), em, den=den, nums=nums)

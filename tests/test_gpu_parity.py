@@ -355,7 +355,8 @@ def test_paper_shape_den_n2(fbx):
     """N2: the paper's Table 1 denominator shape (3022 states, 50,984 arcs, D = 84;
     P:445-457), whose schedule exceeds one SM's shared memory — it runs split
     over a cluster.  Reduced B and N; oracle parity on logZ, posteriors, grad rows."""
-    den, emis = synth.make_paper_shape(seed=6, B=3, N=70)
+    w = synth.make_paper_shape(seed=6, B=3, N=70, L_range=(10, 20))
+    den, emis = w.den, w.emis
     lens = np.array([70, 70, 23], np.int32)
     r = run_fb(fbx, den, emis, lens, post="pdf")
     assert r["g"].info["cluster_C"] >= 2
@@ -364,3 +365,21 @@ def test_paper_shape_den_n2(fbx):
     check_logZ(r["logZ"], ref["logZ"], np.ones(3, bool))
     check_logZ(r["logZb"], ref["logZ"], np.ones(3, bool))
     assert np.abs(r["post"] - ref["post_pdf"]).max() <= TOL_POST
+
+
+def test_paper_shape_lfmmi_n2(fbx):
+    """N2 LF-MMI: paper-shape denominator (cluster kernel) + ≈454-state numerators."""
+    import torch
+
+    w = synth.make_paper_shape(seed=7, B=4, N=90, L_range=(30, 45))
+    lens = np.array([90, 90, 60, 90], np.int32)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(w.emis), dev(lens))
+    torch.cuda.synchronize()
+    ref = oracle.lfmmi_batch(synth.compose(w.nums), synth.compose([w.den]), w.emis, lens)
+    st = st.cpu().numpy()
+    assert (st == 0).all() and (ref["status"] == 0).all()
+    assert np.abs(grad.cpu().numpy() - ref["grad"]).max() <= TOL_GRAD
+    err = np.abs(loss.cpu().numpy() - ref["loss"]) / np.maximum(1, np.abs(ref["logZ_den"]))
+    assert err.max() <= TOL_LOGZ
