@@ -218,6 +218,29 @@ fb_status fb_viterbi(fb_graph g, const float *log_emis, const int32_t *lengths, 
                      size_t workspace_bytes, void *stream);
 
 /*
+ * fb_forward_literal — the paper's own execution strategy, generic in the
+ * semiring: the batch is one
+ * block-diagonal matrix (G == 1: B copies of the shared graph; G == B: graph b
+ * for sequence b), each block augmented with a phony state (arcs s → phony
+ * weighted ω(s), a 1̄ self-loop; emissions 0̄/1̄ past N_b, ledger L8), and
+ * every frame is ONE sparse matrix-vector product x_n = v_n ⊗ Tᵀ x_{n−1}
+ * (Eq. (13)) over the whole batch, one kernel launch per frame, N_max + 1
+ * frames, float64, no normalisation.  score[b] = x_{N_max}(phony_b):
+ *   FB_SEMIRING_LOG       log Z_b (natural log; equals fb_forward's logZ),
+ *   FB_SEMIRING_TROPICAL  the best-path score (equals fb_viterbi's score),
+ *   FB_SEMIRING_PROB      Z_b in the probability domain (exp of weights and
+ *                         emissions; underflows to 0 on long inputs).
+ * Sequences with N_b ∉ [1, N_max] get the semiring's 0̄.  A reference /
+ * A/B baseline for the fused kernels, not a fast path.  workspace ≥
+ * fb_literal_workspace_bytes(g, B) (two batch vectors).
+ */
+enum { FB_SEMIRING_LOG = 0, FB_SEMIRING_TROPICAL = 1, FB_SEMIRING_PROB = 2 };
+size_t fb_literal_workspace_bytes(fb_graph g, int32_t B);
+fb_status fb_forward_literal(fb_graph g, int32_t semiring, const float *log_emis, const int32_t *lengths,
+                             int32_t B, int32_t N_max, double *score, void *workspace, size_t workspace_bytes,
+                             void *stream);
+
+/*
  * Kernel timing (tracing).  When enabled, every kernel the library launches is
  * bracketed by cudaEventRecord on the stream it is launched on.
  * fb_profile_collect synchronises those events and returns, per kernel name,

@@ -25,7 +25,8 @@ from ._lib import EXPORTS, lib  # noqa: F401
 
 __all__ = [
     "FBError", "Graph", "fb_forward", "fb_backward", "fb_posteriors", "lfmmi_loss_grad", "workspace_bytes",
-    "fb_viterbi", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
+    "fb_viterbi", "fb_forward_literal", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
+    "SEMIRING_LOG", "SEMIRING_TROPICAL", "SEMIRING_PROB",
     "SEQ_OK", "SEQ_EMPTY_LATTICE", "SEQ_NONFINITE_INPUT", "SEQ_BAD_LENGTH",
     "GRAPH_DEFAULT", "GRAPH_FORCE_EXACT", "GRAPH_FORCE_FACTORED", "GRAPH_CLUSTER",
 ]
@@ -262,6 +263,26 @@ def fb_viterbi(g: Graph, emis, lengths):
                             _dev(st, torch.int32, "status"), _dev(ws, torch.uint8, "workspace"), ws.numel(),
                             _stream()), "fb_viterbi")
     return score, path, st
+
+
+SEMIRING_LOG, SEMIRING_TROPICAL, SEMIRING_PROB = 0, 1, 2
+
+
+def fb_forward_literal(g: Graph, emis, lengths, semiring: int = SEMIRING_LOG):
+    """The paper's literal strategy (N4): one block-diagonal batch SpMV per frame with
+    phony-state padding, in the log / tropical / probability semiring.  Returns score [B] f64."""
+    import torch
+
+    B, N_max, D = emis.shape
+    dev = emis.device
+    nbytes = int(lib().fb_literal_workspace_bytes(g.handle, B))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    _check(lib().fb_forward_literal(g.handle, int(semiring), _dev(emis, torch.float32, "emis"),
+                                    _dev(lengths, torch.int32, "lengths"), B, N_max,
+                                    _dev(score, torch.float64, "score"), _dev(ws, torch.uint8, "workspace"),
+                                    ws.numel(), _stream()), "fb_forward_literal")
+    return score
 
 
 def profile_enable(on: bool = True) -> None:

@@ -28,6 +28,8 @@ _SIGS = {
     "lfmmi_loss_grad": (c_i32, [c_p, c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "fb_viterbi_workspace_bytes": (c_sz, [c_p, c_i32, c_i32]),
     "fb_viterbi": (c_i32, [c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_sz, c_p]),
+    "fb_literal_workspace_bytes": (c_sz, [c_p, c_i32]),
+    "fb_forward_literal": (c_i32, [c_p, c_i32, c_p, c_p, c_i32, c_i32, c_p, c_p, c_sz, c_p]),
     "fb_profile_enable": (None, [c_i32]),
     "fb_profile_reset": (None, []),
     "fb_profile_collect": (c_i32, [c_p, c_p, c_p, c_i32, c_p]),

@@ -568,6 +568,8 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         final2[i] = (float)((double)log_final[i] * kLog2e);
     }
     RowLists in0, out0;  // member 0's arc lists (cluster plan of a shared graph)
+    std::vector<int> lit_row_off(G), lit_ptr(1, 0), lit_src, lit_inst(G + 1, 0);
+    std::vector<double> lit_w;
     for (int g = 0; g < G; ++g) {
         const int s0 = state_offsets[g], K = state_offsets[g + 1] - s0;
         RowLists in, outl;
@@ -641,6 +643,21 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         slot_sptr.push_back((int)slot_states.size());
         slot_off[g + 1] = slot_off[g] + local;
         gr.pm.U_max = std::max(gr.pm.U_max, local);
+        // literal batch matrix rows: in-arcs of every state, then the phony state's row
+        lit_row_off[g] = (int)lit_ptr.size() - 1;
+        for (int j = 0; j < K; ++j) {
+            for (int a2 = in.ptr[j]; a2 < in.ptr[j + 1]; ++a2) { lit_src.push_back(in.other[a2]); lit_w.push_back(in.w[a2]); }
+            lit_ptr.push_back((int)lit_src.size());
+        }
+        for (int k = 0; k < K; ++k)
+            if (!(std::isinf(log_final[s0 + k]) && log_final[s0 + k] < 0)) {
+                lit_src.push_back(k);
+                lit_w.push_back(log_final[s0 + k]);
+            }
+        lit_src.push_back(K);
+        lit_w.push_back(0.0);
+        lit_ptr.push_back((int)lit_src.size());
+        lit_inst[g + 1] = lit_inst[g] + K + 1;
         if (G == 1) { in0 = std::move(in); out0 = std::move(outl); }
     }
     gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
@@ -695,6 +712,8 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         return o;
     };
     SO of = put_sched(hf), ob = put_sched(hb), ov = put_sched(hv);
+    size_t o_lro = pk.put(lit_row_off), o_lp = pk.put(lit_ptr), o_ls = pk.put(lit_src), o_lw = pk.put(lit_w),
+           o_li = pk.put(lit_inst);
     SO ocf{}, ocb{};
     size_t o_cpo = 0, o_cpl = 0, o_cpe = 0, o_cpd = 0, o_cdf = 0, o_cds = 0, o_ci2 = 0, o_cf2 = 0, o_cpq = 0,
            o_fp = 0, o_fs = 0, o_fw = 0, o_bp = 0, o_bs = 0, o_bw = 0;
@@ -754,6 +773,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     set_sched(gr.fwd, of);
     set_sched(gr.bwd, ob);
     set_sched(gr.vit, ov);
+    gr.lit.row_off = (const int *)P(o_lro); gr.lit.ptr = (const int *)P(o_lp); gr.lit.src = (const int *)P(o_ls);
+    gr.lit.w = (const double *)P(o_lw); gr.lit.inst_off = (const int *)P(o_li);
+    gr.lit.g1 = G == 1; gr.lit.K1 = gr.K_max + 1; gr.lit.inst_total = lit_inst[G];
     if (cp_ok) {
         CPlan &c = gr.cp;
         set_sched(c.fwd, ocf);

@@ -90,6 +90,34 @@ struct CPlan {
     const float *fw2 = nullptr, *bw2 = nullptr;
 };
 
+#ifdef __CUDACC__
+#define FBX_HD2 __host__ __device__
+#else
+#define FBX_HD2
+#endif
+// The paper's literal batch matrix (fb_literal.cu): per member, the in-arc
+// lists of its K_g states plus a phony state K_g (arcs s → phony weighted ω(s),
+// a 1̄ self-loop; ledger L8).  Instance b (sequence b) owns rows
+// [inst_off(b), inst_off(b) + K_b + 1) of the batch vector.
+struct LitPlan {
+    const int *row_off = nullptr;   // [G] member g's first row in ptr
+    const int *ptr = nullptr;       // [Σ_g (K_g + 1) + 1]
+    const int *src = nullptr;       // local source ids (K_g = the phony state)
+    const double *w = nullptr;      // natural-log weights (ω for phony arcs, 0 for its self-loop)
+    const int *inst_off = nullptr;  // G == B: [B + 1] = state_off[b] + b
+    int g1 = 1, K1 = 0;             // G == 1: every instance has K + 1 rows
+    long long inst_total = 0;       // G == B: Σ_b (K_b + 1)
+    FBX_HD2 long long rows_per_batch(int B) const { return g1 ? (long long)B * K1 : inst_total; }
+#ifdef __CUDACC__
+    __device__ void locate(long long r, int B, int &b, int &j) const {
+        if (g1) { b = (int)(r / K1); j = (int)(r - (long long)b * K1); return; }
+        int lo = 0, hi = B;  // largest b with inst_off[b] <= r
+        while (hi - lo > 1) { const int m = (lo + hi) >> 1; if (inst_off[m] <= r) lo = m; else hi = m; }
+        b = lo; j = (int)(r - inst_off[lo]);
+    }
+#endif
+};
+
 struct Graph {
     int G = 0, K_tot = 0, D = 0, T = 0, W = 0, spt = 1, mode = 0;
     int mask_fwd = 0, mask_bwd = 0;  // any state ever masked by the viability distances
@@ -110,6 +138,7 @@ struct Graph {
     int vit_ok = 0;   // the Viterbi schedule fits shared memory
     PdfMap pm;
     CPlan cp;         // cluster plan (k_fbc); cp.ok == 0: one CTA per sequence (k_fb)
+    LitPlan lit;      // the paper's literal block-diagonal strategy (fb_literal.cu, N4)
     int legacy_ok = 1; // the one-CTA-per-sequence kernels fit (else only the cluster path runs)
     void *block = nullptr;
     size_t block_bytes = 0;

@@ -1,0 +1,110 @@
+"""N4: the paper's literal execution strategy (block-diagonal batch SpMV per
+frame with phony-state padding) in three semirings,
+through the C-ABI, against the float64 oracle and against the fused kernels."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2112_00709_b200 import synth
+from tests import helpers
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fbx():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    from paper_2112_00709_b200 import build
+
+    build.build()
+    import paper_2112_00709_b200 as fbx
+
+    fbx.lib()
+    return fbx
+
+
+def dev(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def literal(fbx, graph, emis, lengths, sr, flags=0):
+    import torch
+
+    g = fbx.Graph.from_host(graph, flags)
+    s = fbx.fb_forward_literal(g, dev(emis.astype(np.float32)), dev(lengths.astype(np.int32)), sr)
+    torch.cuda.synchronize()
+    return s.cpu().numpy()
+
+
+def test_log_semiring_c1_composed(fbx):
+    """G = B block-diagonal batch of 100 dense K = 3 graphs (C1)."""
+    ws = [synth.make_c1(s) for s in range(100)]
+    g = synth.compose([w.den for w in ws])
+    emis = np.concatenate([w.emis for w in ws])
+    lens = np.full(100, 6, np.int32)
+    lens[::7] = 3  # ragged: phony padding must reproduce the per-length result
+    got = literal(fbx, g, emis, lens, fbx.SEMIRING_LOG)
+    ref = oracle.fb_batch(g, emis, lens, post=False)["logZ"]
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_log_semiring_den_vs_oracle_and_fused(fbx):
+    """G = 1 shared denominator (B copies in the block-diagonal batch)."""
+    import torch
+
+    w = synth.make_c3(seed=31, B=5, N=40, K=700, nnz=4000)
+    lens = np.array([40, 1, 17, 40, 29], np.int32)
+    got = literal(fbx, w.den, w.emis, lens, fbx.SEMIRING_LOG)
+    ref = oracle.fb_batch(w.den, w.emis, lens, post=False)["logZ"]
+    assert (np.abs(got - ref) / np.abs(ref)).max() <= 1e-12
+    g = fbx.Graph.from_host(w.den)
+    logZ, _, _, st = fbx.fb_forward(g, dev(w.emis), dev(lens))
+    torch.cuda.synchronize()
+    assert (np.abs(logZ.cpu().numpy() - got) / np.abs(got)).max() <= 1e-5
+
+
+def test_log_semiring_numerators(fbx):
+    w = synth.make_c2(seed=2, B=12)
+    g = synth.compose(w.nums)
+    got = literal(fbx, g, w.emis, w.lengths, fbx.SEMIRING_LOG)
+    ref = oracle.fb_batch(g, w.emis, w.lengths, post=False)["logZ"]
+    assert (np.abs(got - ref) / np.abs(ref)).max() <= 1e-12
+
+
+def test_tropical_semiring_is_viterbi(fbx):
+    w = synth.make_c2(seed=3, B=8)
+    g = synth.compose(w.nums)
+    got = literal(fbx, g, w.emis, w.lengths, fbx.SEMIRING_TROPICAL)
+    ref = oracle.viterbi_batch(g, w.emis, w.lengths)["score"]
+    assert np.abs(got - ref).max() <= 1e-9 * np.abs(ref).max()
+    ws = [synth.make_c1(s) for s in range(20)]
+    g1 = synth.compose([x.den for x in ws])
+    e1 = np.concatenate([x.emis for x in ws])
+    l1 = np.full(20, 6, np.int32)
+    got1 = literal(fbx, g1, e1, l1, fbx.SEMIRING_TROPICAL)
+    assert np.abs(got1 - oracle.viterbi_batch(g1, e1, l1)["score"]).max() <= 1e-12
+
+
+def test_prob_semiring_equals_exp_logZ_and_underflows(fbx):
+    """Probability domain: exp(logZ) on short inputs; on the AC6 input (N = 1000,
+    φ ∈ [−100, −50]) it underflows to exactly 0 while the log semiring stays
+    finite and matches the oracle — the paper's reason for the log domain."""
+    ws = [synth.make_c1(s) for s in range(10)]
+    g = synth.compose([w.den for w in ws])
+    emis = np.concatenate([w.emis for w in ws])
+    lens = np.full(10, 6, np.int32)
+    got = literal(fbx, g, emis, lens, fbx.SEMIRING_PROB)
+    ref = np.exp(oracle.fb_batch(g, emis, lens, post=False)["logZ"])
+    assert (np.abs(got - ref) / ref).max() <= 1e-12
+    lr = helpers.left_to_right(10)
+    rng = np.random.default_rng(6)
+    e = rng.uniform(-100, -50, (1, 1000, 10)).astype(np.float32)
+    L = np.array([1000], np.int32)
+    assert literal(fbx, lr, e, L, fbx.SEMIRING_PROB)[0] == 0.0
+    lz = literal(fbx, lr, e, L, fbx.SEMIRING_LOG)[0]
+    ref = oracle.fb_batch(lr, e, L, post=False)["logZ"][0]
+    assert np.isfinite(lz) and abs(lz - ref) <= 1e-12 * abs(ref)
