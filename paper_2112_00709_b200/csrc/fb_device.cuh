@@ -235,18 +235,17 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
         uint32_t ia = cur + 128 + lane * 4;
         uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
         if (MODE == MODE_FACTORED) {
-            float a0 = 0.f, a1 = 0.f;
+            float2 a2 = make_float2(0.f, 0.f);  // two accumulators, one packed FFMA2 per arc pair
 #pragma unroll 2
             for (int s = 0; s < L2; ++s) {
                 const uint32_t ix = lds_u32(ia);
                 const float2 w2 = lds_f2(wa);
                 const float p0 = lds_v(a_p + (ix & 0xFFFFu), 0.f), p1 = lds_v(a_p + (ix >> 16), 0.f);
-                a0 = fmaf(p0, w2.x, a0);
-                a1 = fmaf(p1, w2.y, a1);
+                a2 = __ffma2_rn(make_float2(p0, p1), w2, a2);
                 ia += 128;
                 wa += 256;
             }
-            float acc = a0 + a1;
+            float acc = a2.x + a2.y;
             if (lg) {
                 for (int o = 1; o < (1 << lg); o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             }
@@ -361,7 +360,7 @@ inline __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int
 // MODEX: MODE_FACTORED / MODE_EXACT / MODE_RAW, or kModeFactoredTma (factored
 // arithmetic with φ rows staged through TMA).
 constexpr int kModeFactoredTma = 4;
-template <bool BWD, int MODEX, int SPT>
+template <bool BWD, int MODEX, int SPT, int TT>
 __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     constexpr bool TMA = MODEX == kModeFactoredTma;
     constexpr int MODE = TMA ? (int)MODE_FACTORED : MODEX;
@@ -371,7 +370,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Graph &G = a.g;
     const int gi = (G.G == 1) ? 0 : b;
-    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = T >> 5;
+    constexpr int T = TT, W = TT >> 5;  // the launch uses exactly TT threads (compile-time offsets)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int s0 = G.state_off[gi];
     const int K = G.state_off[gi + 1] - s0;
     const int N = a.lengths[b];
@@ -741,7 +741,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 template <bool BWD, int MODEX, int SPT, int MAXT>
 __global__ void __launch_bounds__(MAXT, (MAXT >= 512 ? 1 : (MAXT == 256 ? 2 : 7))) k_fb(const FBArgs a) {
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-        fb_sequence<BWD, MODEX, SPT>(a, b);
+        fb_sequence<BWD, MODEX, SPT, MAXT>(a, b);
         __syncthreads();  // shared memory is reused by the next sequence
     }
 }

@@ -539,12 +539,13 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     // dependent chains, so they get ~4 arcs per thread to cut per-frame latency.
     int T;
     if (gr.mode == MODE_FACTORED)
-        T = gr.nnz_max >= 16384 ? 1024 : std::min(1024, std::max(64, pow2ceil((gr.nnz_max + 15) / 16)));
+        T = gr.nnz_max >= 16384 ? 1024 : std::min(1024, std::max(128, pow2ceil((gr.nnz_max + 15) / 16)));
     else
         T = std::min(1024, std::max(128, pow2ceil((gr.nnz_max + 7) / 8)));
-    if (const char *e = std::getenv("FBX_EXACT_T"); e && gr.mode == MODE_EXACT) T = std::max(32, std::atoi(e));
-    if (const char *e = std::getenv("FBX_FACT_T"); e && gr.mode == MODE_FACTORED) T = std::max(32, std::atoi(e));
+    if (const char *e = std::getenv("FBX_EXACT_T"); e && gr.mode == MODE_EXACT) T = std::max(128, std::atoi(e));
+    if (const char *e = std::getenv("FBX_FACT_T"); e && gr.mode == MODE_FACTORED) T = std::max(128, std::atoi(e));
     T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
+    T = std::min(1024, pow2ceil(T));  // T ∈ {128, 256, 512, 1024}: the kernels' compile-time CTA size
     int spt = (gr.K_max + T - 1) / T;
     spt = spt <= 4 ? spt : (spt <= 6 ? 6 : 8);  // instantiated: 1, 2, 3, 4, 6, 8
     if ((gr.K_max + T - 1) / T > kMaxSPT) return FB_ERR_UNSUPPORTED;

@@ -22,13 +22,14 @@ static KFn pick_spt(int spt) {
     }
 }
 
-// MAXT = 128 variants (six CTAs per SM) and 256 (two per SM) for small CTAs; 1024 otherwise.
+// The CTA size T ∈ {128, 256, 512, 1024} is a compile-time constant of the
+// kernel (MAXT == T): 128 (seven CTAs per SM), 256 (two per SM), 512 (≤ 128
+// registers per thread), 1024.
 template <bool BWD, int MODE>
 KFn pick_fb(int spt, int T) {
     if (T <= 128) return pick_spt<BWD, MODE, 128>(spt);
     if (T <= 256) return pick_spt<BWD, MODE, 256>(spt);
-    if constexpr (MODE == MODE_FACTORED || MODE == kModeFactoredTma)
-        if (T <= 512) return pick_spt<BWD, MODE, 512>(spt);  // ≤ 128 registers per thread
+    if (T <= 512) return pick_spt<BWD, MODE, 512>(spt);
     return pick_spt<BWD, MODE, 1024>(spt);
 }
 
