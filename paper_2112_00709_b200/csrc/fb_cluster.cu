@@ -72,6 +72,16 @@ __device__ __forceinline__ void mbar_wait_cl(uint32_t a, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Wait for an mbarrier phase with a suspend-time hint: the warp sleeps in
+// hardware until the phase completes instead of re-issuing the probe.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred P1;\n"
+        "WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+        " @!P1 bra WAITS_%=;\n}\n" ::"r"(a),
+        "r"(parity), "r"(1000000u)
+        : "memory");
+}
 __device__ __forceinline__ void cpa16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -347,12 +357,6 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (t >= Ns[s]) continue;  // CTA-uniform
-            if (a.lat) {
-                float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * K;
-#pragma unroll
-                for (int k = 0; k < SPT; ++k)
-                    if (origk[k] >= 0) latn[origk[k]] = h[k][s] * LN2;
-            }
             float mx = u[0][s];
 #pragma unroll
             for (int k = 1; k < SPT; ++k) mx = fmaxf(mx, u[k][s]);
@@ -388,6 +392,19 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                     sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 4) * 4, ts);
                 }
             }
+        }
+    };
+    // α̂/β̂ rows of frame t to HBM — issued after the frame has been shipped, so the
+    // proxy fence before the bulk copies does not wait for these stores
+    auto store_lat = [&](int t, float (&h)[SPT][S]) {
+        if (!a.lat) return;
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            if (t >= Ns[s]) continue;
+            float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * K;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k)
+                if (origk[k] >= 0) latn[origk[k]] = h[k][s] * LN2;
         }
     };
     // warp 0: per-warp reductions → this part's extras slot of buffer t; lane 0 ships the frame
@@ -476,6 +493,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         fence_async_smem();
         __syncthreads();
         send(0);
+        store_lat(0, h);
     }
 
     // ---- frames 1 … Tmax−1 (+ one flush step t = Tmax for the last posterior rows)
@@ -488,7 +506,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             if (want_post) load_alpha(t);
             emis_issue(t + 1);
         }
-        mbar_wait(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
+        mbar_wait_sleep(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
         const uint32_t up = a_u(t - 1);
         if (!last) {  // p = 2^u of the other parts' rows
             for (int e = 4 * tid; e < Kint * S; e += 4 * T) {
@@ -618,6 +636,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         fence_async_smem();
         __syncthreads();  // u / p rows and reductions of frame t complete
         send(t);
+        store_lat(t, h);
     }
 
     // ---- termination: logZ = C + ⊕_k α̂ ⊗ ω (fwd) / logZ_β = D + ⊕_k π ⊗ β̂_0 ⊗ v_0 (bwd);

@@ -496,12 +496,12 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     // α̂ of frame n as stored (float natural log, or the raw float64 log2 lattice);
     // converted to log2 at use so the load is not waited on at issue
     auto load_alpha = [&](int n, V *v) {
-        const size_t ro = lat_base + (size_t)min(max(n, 0), N - 1) * K;
+        const size_t ro = lat_base + (size_t)min(max(n, 0), N - 1) * K + tid;  // one base pointer, immediate offsets
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
-            const int j = min(tid + k * T, K - 1);
-            if (RAW) v[k] = (V)__ldg(a.alpha64 + ro + j);
-            else v[k] = (V)__ldg(a.alpha + ro + j);
+            const bool in = tid + k * T < K;
+            if (RAW) v[k] = in ? (V)__ldg(a.alpha64 + ro + k * T) : (V)0;
+            else v[k] = in ? (V)__ldg(a.alpha + ro + k * T) : (V)0;
         }
     };
     // viable(k, n): forward — a final state is reachable in the N-1-n remaining
