@@ -116,7 +116,9 @@ struct VS<4> {
 
 // Phase A over this warp's slices (Sched layout, fb_internal.h) with S-float
 // gathered elements: lane l reduces one row segment for all S sequences.
-template <int S>
+// NOP: the gathered array is u itself (log2) and each element is exponentiated
+// on the fly (one MUFU ex2 per sequence-arc) — used when p = 2^u does not fit.
+template <int S, bool NOP>
 __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uint32_t a_p, uint32_t a_part) {
     for (int q = 0; q < nsl; ++q) {
         const uint32_t h = lds_u32(cur + lane * 4);
@@ -133,6 +135,10 @@ __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uin
             float p0[S], p1[S];
             VS<S>::ld(a_p + (ix & 0xFFFFu), p0);
             VS<S>::ld(a_p + (ix >> 16), p1);
+            if (NOP) {
+#pragma unroll
+                for (int i = 0; i < S; ++i) { p0[i] = ex2(p0[i]); p1[i] = ex2(p1[i]); }
+            }
 #pragma unroll
             for (int i = 0; i < S; ++i) {
                 a0[i] = fmaf(p0[i], w2.x, a0[i]);
@@ -171,7 +177,7 @@ static __device__ __noinline__ float exact_row_c(const int *ptr, const int *src,
 // Combine (m, s) log-sum-exp pairs (m in log2, s ≥ 0) in a fixed order.
 __device__ __forceinline__ void lse2(float &m, float &s, float m2, float s2) { lse_combine<float>(m, s, m2, s2); }
 
-template <bool BWD, int S, int SPT, int T>
+template <bool BWD, int S, int SPT, int T, bool NOP>
 __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int W = T / 32;
@@ -187,7 +193,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     const Sched &SC = BWD ? P.bwd : P.fwd;
     const bool want_post = BWD && a.post_kind != POST_NONE;
     const bool pdf_post = want_post && a.post_kind != POST_STATE;
-    const CLayout L = cl_layout(SC.bytes_max, Kint, P.Kc_max, P.Dc_max, S, C, W, BWD);
+    const CLayout L = cl_layout(SC.bytes_max, Kint, P.Kc_max, P.Dc_max, S, C, W, BWD, NOP);
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t a_rec = sb + (uint32_t)L.rec, a_u0 = sb + (uint32_t)L.u, a_p = sb + (uint32_t)L.p;
     const uint32_t a_part = sb + (uint32_t)L.part, a_gbuf = sb + (uint32_t)L.gbuf, a_pq = sb + (uint32_t)L.pq;
@@ -351,7 +357,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) pv[s] = ex2(u[k][s]);
                 VS<S>::st(ub + (uint32_t)((k0 + j) * S) * 4, u[k]);
-                VS<S>::st(a_p + (uint32_t)((k0 + j) * S) * 4, pv);
+                if (!NOP) VS<S>::st(a_p + (uint32_t)((k0 + j) * S) * 4, pv);
             }
         }
 #pragma unroll
@@ -508,7 +514,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         }
         mbar_wait_sleep(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
         const uint32_t up = a_u(t - 1);
-        if (!last) {  // p = 2^u of the other parts' rows
+        if (!last && !NOP) {  // p = 2^u of the other parts' rows
             for (int e = 4 * tid; e < Kint * S; e += 4 * T) {
                 if (e >= own0 && e < own1) continue;
                 float v[4];
@@ -560,7 +566,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 }
             }
         }
-        if (!last) phase_a_vec<S>(mysl, nsl, lane, a_p, a_part);
+        if (!last) phase_a_vec<S, NOP>(mysl, nsl, lane, NOP ? up : a_p, a_part);
         cpa_wait1();
         __syncthreads();  // part rows, γ rows, step-t emissions complete
         // pdf-level rows of frame t−1 for this part's pdf range (ascending states, ledger L9)
@@ -578,6 +584,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                     row[d] = sgn * acc;
                 }
             }
+            if (NOP) __syncthreads();  // γ lives in xbuf, which phase B refills with the next x
         }
         if (last) break;
         // ---- phase B of frame t: y = log2 Σ, emission, lagged normaliser, mask
@@ -691,26 +698,34 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 }
 
 using KFn = void (*)(FBArgs);
-// T = 1024 threads (SPT ≤ 4, ≤ 64 registers) or 512 (SPT ≤ 8, ≤ 128 registers)
-template <bool BWD, int S>
-KFn pick_fbc(int spt, int T) {
+// T = 1024 threads (SPT ≤ 4, ≤ 64 registers) or 512 (SPT ≤ 8, ≤ 128 registers);
+// nop (S = 4 only): no p array
+template <bool BWD, int S, bool NOP>
+static KFn pick_fbc_t(int spt, int T) {
     if (T == 1024) {
         switch (spt) {
-            case 1: return k_fbc<BWD, S, 1, 1024>;
-            case 2: return k_fbc<BWD, S, 2, 1024>;
-            case 3: return k_fbc<BWD, S, 3, 1024>;
-            default: return k_fbc<BWD, S, 4, 1024>;
+            case 1: return k_fbc<BWD, S, 1, 1024, NOP>;
+            case 2: return k_fbc<BWD, S, 2, 1024, NOP>;
+            case 3: return k_fbc<BWD, S, 3, 1024, NOP>;
+            default: return k_fbc<BWD, S, 4, 1024, NOP>;
         }
     }
     switch (spt) {
-        case 1: return k_fbc<BWD, S, 1, 512>;
-        case 2: return k_fbc<BWD, S, 2, 512>;
-        case 3: return k_fbc<BWD, S, 3, 512>;
-        case 4: return k_fbc<BWD, S, 4, 512>;
-        case 6: return k_fbc<BWD, S, 6, 512>;
-        default: return k_fbc<BWD, S, 8, 512>;
+        case 1: return k_fbc<BWD, S, 1, 512, NOP>;
+        case 2: return k_fbc<BWD, S, 2, 512, NOP>;
+        case 3: return k_fbc<BWD, S, 3, 512, NOP>;
+        case 4: return k_fbc<BWD, S, 4, 512, NOP>;
+        case 6: return k_fbc<BWD, S, 6, 512, NOP>;
+        default: return k_fbc<BWD, S, 8, 512, NOP>;
     }
 }
-template KFn pick_fbc<(bool)FBX_BWD, FBX_S>(int, int);
+template <bool BWD, int S>
+KFn pick_fbc(int spt, int T, int nop) {
+    if constexpr (S == 4) {
+        if (nop) return pick_fbc_t<BWD, S, true>(spt, T);
+    }
+    return pick_fbc_t<BWD, S, false>(spt, T);
+}
+template KFn pick_fbc<(bool)FBX_BWD, FBX_S>(int, int, int);
 
 }  // namespace fbx

@@ -322,7 +322,7 @@ bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
 
 // Host image of a CPlan (fb_internal.h).
 struct HostCPlan {
-    int C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0, emis16 = 0;
+    int C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0, emis16 = 0, nop = 0;
     std::vector<int> part_off, pdf_lo, perm, ipdf, idf, ids;
     std::vector<float> ii2, if2;
     std::vector<unsigned> pq;
@@ -339,14 +339,14 @@ struct HostCPlan {
 bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, const std::vector<int> &pdf,
                         const std::vector<int> &dist_fin, const std::vector<int> &dist_start,
                         const std::vector<float> &init2, const std::vector<float> &final2, int C, int S, int Lmax,
-                        HostCPlan &cp, int Tforce = 0) {
+                        HostCPlan &cp, int Tforce = 0, bool nop = false) {
     // 1024 threads (≤ 4 owned states each) unless the part needs more states per thread
     int T = 1024;
     if (const char *e = std::getenv("FBX_CLUSTER_T")) T = std::atoi(e) == 512 ? 512 : 1024;
     if (Tforce) T = Tforce;
     const int W = T / 32;
     cp = HostCPlan();
-    cp.C = C; cp.S = S; cp.T = T;
+    cp.C = C; cp.S = S; cp.T = T; cp.nop = nop;
     std::vector<double> cost(D, 0.0);
     for (int k = 0; k < K; ++k)
         cost[pdf[k]] += (in.ptr[k + 1] - in.ptr[k]) + (out.ptr[k + 1] - out.ptr[k]) + 8.0;
@@ -386,8 +386,8 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
     cp.K_int = (int)cp.perm.size();
     if ((long long)cp.K_int * S * 4 > 65536) return false;  // 16-bit gather offsets
     cp.spt = (cp.Kc_max + T - 1) / T;
-    if (T == 1024 && cp.spt > 4)
-        return build_cluster_plan(in, out, K, D, pdf, dist_fin, dist_start, init2, final2, C, S, Lmax, cp, 512);
+    if (T == 1024 && (cp.spt > 4 || S == 4))  // S = 4 kernels need > 64 registers per thread
+        return build_cluster_plan(in, out, K, D, pdf, dist_fin, dist_start, init2, final2, C, S, Lmax, cp, 512, nop);
     if (cp.spt > 8) return false;
     cp.spt = cp.spt <= 4 ? cp.spt : (cp.spt <= 6 ? 6 : 8);
     const int Ki = cp.K_int;
@@ -452,8 +452,12 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
             if (!build_member_sched(pl, Kc, T, MODE_FACTORED, 4 * S, Lmax, hs, true)) return false;
         }
     }
-    cp.smem_fwd = cl_layout(cp.hf.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, false).total;
-    cp.smem_bwd = cl_layout(cp.hb.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, true).total;
+    cp.smem_fwd = cl_layout(cp.hf.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, false, nop).total;
+    cp.smem_bwd = cl_layout(cp.hb.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, true, nop).total;
+    if (std::getenv("FBX_CLUSTER_DEBUG"))
+        std::fprintf(stderr, "cluster plan C=%d S=%d nop=%d T=%d spt=%d K_int=%d Kc_max=%d rec_fwd=%d rec_bwd=%d smem_fwd=%zu smem_bwd=%zu\n",
+                     C, S, (int)nop, T, cp.spt, cp.K_int, cp.Kc_max, cp.hf.bytes_max, cp.hb.bytes_max, cp.smem_fwd,
+                     cp.smem_bwd);
     return cp.smem_fwd <= (size_t)kSmemLimit && cp.smem_bwd <= (size_t)kSmemLimit;
 }
 
@@ -678,15 +682,17 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
                          (size_t)kSmemLimit);
     const bool want_cluster = (flags & FB_GRAPH_CLUSTER) || std::getenv("FBX_CLUSTER") || !gr.legacy_ok;
     if (G == 1 && gr.mode == MODE_FACTORED && want_cluster) {
-        std::vector<std::pair<int, int>> cand = {{2, 2}, {4, 2}, {8, 2}, {4, 4}, {8, 4}};
+        // (C, S, no-p): single-wave shapes for B = 128 first ((2,2), (4,4): 128 CTAs), then wider clusters
+        struct Cand { int C, S, nop; };
+        std::vector<Cand> cand = {{2, 2, 0}, {4, 4, 0}, {4, 4, 1}, {4, 2, 0}, {8, 2, 0}, {8, 4, 0}, {8, 4, 1}};
         if (const char *e = std::getenv("FBX_CLUSTER")) {
-            int c = 0, sq = 0;
-            if (std::sscanf(e, "%d,%d", &c, &sq) == 2) cand = {{c, sq}};
+            int c = 0, sq = 0, np = 0;
+            if (std::sscanf(e, "%d,%d,%d", &c, &sq, &np) >= 2) cand = {{c, sq, np}};
         }
         for (auto cs : cand) {
-            if (cs.first < 2 || cs.first > 8 || !(cs.second == 2 || cs.second == 4)) continue;
-            if (build_cluster_plan(in0, out0, K_tot, D, pdf, dist_fin, dist_start, init2, final2, cs.first,
-                                   cs.second, 12, hcp)) { cp_ok = true; break; }
+            if (cs.C < 2 || cs.C > 8 || !(cs.S == 2 || cs.S == 4) || (cs.nop && cs.S != 4)) continue;
+            if (build_cluster_plan(in0, out0, K_tot, D, pdf, dist_fin, dist_start, init2, final2, cs.C, cs.S, 12, hcp,
+                                   0, cs.nop != 0)) { cp_ok = true; break; }
         }
     }
     gr.pm.U_tot = slot_off[G];
@@ -727,7 +733,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         o_bp = pk.put(hcp.bptr); o_bs = pk.put(hcp.bsrc); o_bw = pk.put(hcp.bw2);
         CPlan &c = gr.cp;
         c.ok = 1; c.C = hcp.C; c.S = hcp.S; c.T = hcp.T; c.spt = hcp.spt; c.K_int = hcp.K_int;
-        c.Kc_max = hcp.Kc_max; c.Dc_max = hcp.Dc_max; c.emis16 = hcp.emis16;
+        c.Kc_max = hcp.Kc_max; c.Dc_max = hcp.Dc_max; c.emis16 = hcp.emis16; c.nop = hcp.nop;
         c.fwd.bytes_max = hcp.hf.bytes_max; c.fwd.slots_max = hcp.hf.slots_max;
         c.bwd.bytes_max = hcp.hb.bytes_max; c.bwd.slots_max = hcp.hb.slots_max;
     }

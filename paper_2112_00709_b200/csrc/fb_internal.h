@@ -74,6 +74,7 @@ struct PdfMap {
 // (member c = part c's rows); index words are byte offsets into p[K_int][S].
 struct CPlan {
     int ok = 0, C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0;
+    int nop = 0;                        // no p = 2^u array: phase A applies ex2 to the gathered u (smem-bound configs)
     int emis16 = 0;                     // emission segments are 16-byte aligned (D % 4 == 0)
     const int *part_off = nullptr;      // [C+1] internal state offsets
     const int *pdf_lo = nullptr;        // [C+1] part c owns pdfs [pdf_lo[c], pdf_lo[c+1])
@@ -202,16 +203,17 @@ constexpr int kCX = 8;  // floats per (part, sequence) extras slot
 struct CLayout {
     size_t rec, u, ubytes, p, part, gbuf, xbuf, pq, ebuf, red, mbar, total;
 };
-FBX_HD inline CLayout cl_layout(int rec_bytes, int K_int, int Kc_max, int Dc_max, int S, int C, int W, bool pdfpost) {
+FBX_HD inline CLayout cl_layout(int rec_bytes, int K_int, int Kc_max, int Dc_max, int S, int C, int W, bool pdfpost,
+                                bool nop = false) {
     CLayout L;
     size_t o = 0;
     L.rec = o; o += fbx_a16((size_t)rec_bytes);
     L.ubytes = (size_t)K_int * S * 4 + (size_t)C * S * kCX * 4;
     L.u = o; o += 2 * fbx_a16(L.ubytes);
-    L.p = o; o += fbx_a16((size_t)K_int * S * 4);
+    L.p = o; if (!nop) o += fbx_a16((size_t)K_int * S * 4);  // nop: phase A exponentiates u on the fly
     L.part = o; o += fbx_a16((size_t)Kc_max * S * 4);
-    L.gbuf = o; if (pdfpost) o += fbx_a16((size_t)Kc_max * S * 4);
-    L.xbuf = o; if (pdfpost) o += fbx_a16((size_t)Kc_max * S * 4);
+    L.gbuf = o; if (pdfpost && !nop) o += fbx_a16((size_t)Kc_max * S * 4);
+    L.xbuf = o; if (pdfpost) o += fbx_a16((size_t)Kc_max * S * 4);  // nop: γ overwrites x in place (gbuf = xbuf)
     L.pq = o; if (pdfpost) o += fbx_a16((size_t)Dc_max * 4);
     L.ebuf = o; o += 2 * fbx_a16((size_t)S * Dc_max * 4);
     L.red = o; o += fbx_a16((size_t)(W + 2) * S * kCX * 4);

@@ -381,11 +381,11 @@ static fb_status check_launch(const char *what) {
 }
 
 template <bool BWD, int S>
-KFn pick_fbc(int spt, int T);
-extern template KFn pick_fbc<false, 2>(int, int);
-extern template KFn pick_fbc<false, 4>(int, int);
-extern template KFn pick_fbc<true, 2>(int, int);
-extern template KFn pick_fbc<true, 4>(int, int);
+KFn pick_fbc(int spt, int T, int nop);
+extern template KFn pick_fbc<false, 2>(int, int, int);
+extern template KFn pick_fbc<false, 4>(int, int, int);
+extern template KFn pick_fbc<true, 2>(int, int, int);
+extern template KFn pick_fbc<true, 4>(int, int, int);
 
 // Does this launch run the cluster-batched kernel k_fbc (fb_cluster.cu)?
 static bool use_cluster(bool bwd, const FBArgs &a, bool raw) {
@@ -405,10 +405,10 @@ static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
     const CPlan &P = G.cp;
     FBArgs aa = a;
     aa.tma = (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0);  // 16-byte emission copies
-    KFn fn = bwd ? (P.S == 4 ? pick_fbc<true, 4>(P.spt, P.T) : pick_fbc<true, 2>(P.spt, P.T))
-                 : (P.S == 4 ? pick_fbc<false, 4>(P.spt, P.T) : pick_fbc<false, 2>(P.spt, P.T));
+    KFn fn = bwd ? (P.S == 4 ? pick_fbc<true, 4>(P.spt, P.T, P.nop) : pick_fbc<true, 2>(P.spt, P.T, 0))
+                 : (P.S == 4 ? pick_fbc<false, 4>(P.spt, P.T, P.nop) : pick_fbc<false, 2>(P.spt, P.T, 0));
     const size_t sm = cl_layout(bwd ? P.bwd.bytes_max : P.fwd.bytes_max, P.K_int, P.Kc_max, P.Dc_max, P.S, P.C,
-                                P.T / 32, bwd).total;
+                                P.T / 32, bwd, P.nop != 0).total;
     cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
     cudaLaunchConfig_t cfg;

@@ -298,7 +298,7 @@ def test_viterbi_c3_den(fbx):
 
 # ------------------------------------------------------------------ cluster-batched kernel (k_fbc)
 
-@pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2"])
+@pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2", "4,4,1"])
 def test_cluster_configs_vs_oracle(fbx, cs, monkeypatch):
     """Every (C CTAs, S sequences) cluster configuration of a shared factored
     graph against the oracle: logZ (both directions), α̂ + scale, state and pdf
@@ -307,7 +307,7 @@ def test_cluster_configs_vs_oracle(fbx, cs, monkeypatch):
     w = synth.make_c4(seed=21, B=5, N=48, K=1500, nnz=10000, D=1000, kind="softmax4")
     lens = np.array([48, 1, 30, 48, 17], np.int32)
     r = run_fb(fbx, w.den, w.emis, lens)
-    C, S = (int(x) for x in cs.split(","))
+    C, S = (int(x) for x in cs.split(",")[:2])
     assert (r["g"].info["cluster_C"], r["g"].info["cluster_S"]) == (C, S)
     ref = oracle.fb_batch(w.den, w.emis, lens, alpha=True, post=True, post_pdf=True)
     assert (r["st"] == 0).all()
