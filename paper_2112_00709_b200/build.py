@@ -13,7 +13,9 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libfb.so")
+LIB = os.environ.get("FBX_LIB_OUT") or os.path.join(HERE, "libfb.so")  # FBX_LIB_OUT: experiment builds
+EXTRA = os.environ.get("FBX_EXTRA_FLAGS", "").split()  # e.g. -DFBX_CTIMING (instrumented experiment builds)
+OBJ_TAG = os.environ.get("FBX_OBJ_TAG", "")
 SOURCES = ["fb_graph.cpp", "fb_kernels.cu", "fb_inst.cu", "fb_cluster.cu", "fb_literal.cu"]
 # fb_inst.cu is compiled once per (direction, mode): the k_fb instantiation sets
 INST = [(bwd, mode) for bwd in (0, 1) for mode in (0, 1, 2, 4)]
@@ -46,9 +48,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     cmds, objs = [], []
     for src, obj, extra in _units():
-        obj = os.path.join(CSRC, obj)
+        obj = os.path.join(CSRC, OBJ_TAG + obj)
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
-               *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+               *extra, *EXTRA, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu") and verbose:
             cmd[1:1] = ["-Xptxas", "-v"]
         cmds.append(cmd)

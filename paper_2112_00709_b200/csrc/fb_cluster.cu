@@ -416,7 +416,29 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     // warp 0: per-warp reductions → this part's extras slot of buffer t; lane 0 ships the frame
     auto send = [&](int t) {
         if (warp != 0) return;
-        if (lane < S) {
+        if constexpr (S == 2) {
+            // lane w < W holds warp w's partials: one warp-wide max (REDUX) and one shuffle
+            // sum per sequence (max-first log-sum-exp instead of a serial chain over W warps;
+            // the register-saturated S = 4 kernels keep the one-lane-per-sequence loop)
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t r = a_red + (uint32_t)((lane * S + s) * kCX) * 4;
+                const float mx = warp_max_fast(lane < W ? lds_v(r, 0.f) : NEG_INF);
+                float zm = NEG_INF, zs = 0.f;
+                if (want_post) {
+                    const float pm = lane < W ? lds_v(r + 4, 0.f) : NEG_INF;
+                    const float ps = lane < W ? lds_v(r + 8, 0.f) : 0.f;
+                    zm = warp_max_fast(pm);
+                    zs = warp_sum((pm == NEG_INF) ? 0.f : ps * ex2(pm - zm));
+                }
+                if (lane == s) {
+                    const uint32_t x = a_x(t, cr, s);
+                    sts_v(x, mx);
+                    sts_v(x + 4, zm);
+                    sts_v(x + 8, zs);
+                }
+            }
+        } else if (lane < S) {
             const int s = lane;
             float mx = NEG_INF, zm = NEG_INF, zs = 0.f;
             for (int w = 0; w < W; ++w) {
