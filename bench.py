@@ -302,7 +302,7 @@ def run_ours(args, rank, world, local):
     e2e = None
     if rank == 0 or world > 1:
         emis_h = torch.from_numpy(w.emis).pin_memory()
-        lens_h = torch.from_numpy(w.lengths)
+        lens_h = torch.from_numpy(w.lengths).pin_memory()
         bufs = {}
         for _ in range(2):
             fbx.lfmmi_loss_grad_host(num, den, emis_h, lens_h, bufs)
@@ -310,6 +310,7 @@ def run_ours(args, rank, world, local):
         k2 = max(3, min(args.steps, 10))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
+        bufs["copy_stream"].wait_event(e0)  # the first upload starts inside the timed region
         for _ in range(k2):
             out = fbx.lfmmi_loss_grad_host(num, den, emis_h, lens_h, bufs)
             if world > 1:

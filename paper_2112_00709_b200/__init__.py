@@ -224,27 +224,53 @@ def lfmmi_loss_grad(num: Graph, den: Graph, emis, lengths, grad=None, workspace=
 def lfmmi_loss_grad_host(num: Graph, den: Graph, emis_host, lengths_host, bufs: dict):
     """End-to-end call with HOST inputs: pinned φ and lengths are copied to the
     device, lfmmi_loss_grad runs, and the totals (and per-utterance loss) are
-    copied back.  `bufs` caches the device buffers between calls."""
+    copied back.  `bufs` caches the device buffers between calls.
+
+    Consecutive calls are pipelined: the upload of a call's φ runs on a copy
+    stream into one of two device buffers while the previous call's kernels are
+    still running (its buffer is reused only after the call two steps back has
+    finished reading it), so a training loop is bound by max(PCIe, compute)
+    rather than their sum.  Every call still uploads its own inputs and reads its
+    own results back: the returned pinned tensor [Σ loss, Σ N_b, Σ logZ_num,
+    Σ logZ_den, n_bad, loss_0 … loss_{B−1}] is valid after the stream synchronises
+    and stays valid until the call after next (two output buffers alternate)."""
     import torch
 
     B, N_max, D = emis_host.shape
     dev = torch.device("cuda", torch.cuda.current_device())
     if "emis" not in bufs:
-        bufs["emis"] = torch.empty((B, N_max, D), dtype=torch.float32, device=dev)
-        bufs["lengths"] = torch.empty(B, dtype=torch.int32, device=dev)
+        bufs["emis"] = [torch.empty((B, N_max, D), dtype=torch.float32, device=dev) for _ in range(2)]
+        bufs["lengths"] = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(2)]
         bufs["grad"] = torch.empty((B, N_max, D), dtype=torch.float32, device=dev)
         bufs["ws"] = torch.empty(workspace_bytes(num, den, B, N_max), dtype=torch.uint8, device=dev)
         bufs["loss"] = torch.empty(B, dtype=torch.float64, device=dev)
         bufs["totals"] = torch.empty(5, dtype=torch.float64, device=dev)
         bufs["status"] = torch.empty(B, dtype=torch.int32, device=dev)
-        bufs["out"] = torch.empty(5 + B, dtype=torch.float64).pin_memory()
-    bufs["emis"].copy_(emis_host, non_blocking=True)
-    bufs["lengths"].copy_(lengths_host, non_blocking=True)
-    lfmmi_loss_grad(num, den, bufs["emis"], bufs["lengths"], bufs["grad"], bufs["ws"], bufs["loss"], bufs["totals"],
-                    bufs["status"])
-    bufs["out"][:5].copy_(bufs["totals"], non_blocking=True)
-    bufs["out"][5:].copy_(bufs["loss"], non_blocking=True)
-    return bufs["out"]
+        bufs["out"] = [torch.empty(5 + B, dtype=torch.float64).pin_memory() for _ in range(2)]
+        bufs["copy_stream"] = torch.cuda.Stream(device=dev)
+        bufs["free"] = [None, None]  # event: the compute that last read buffer i has finished
+        bufs["i"] = 0
+    i = bufs["i"] & 1
+    bufs["i"] += 1
+    comp = torch.cuda.current_stream(dev)
+    cs = bufs["copy_stream"]
+    with torch.cuda.stream(cs):
+        if bufs["free"][i] is not None:
+            cs.wait_event(bufs["free"][i])
+        bufs["emis"][i].copy_(emis_host, non_blocking=True)
+        bufs["lengths"][i].copy_(lengths_host, non_blocking=True)
+        copied = torch.cuda.Event()
+        copied.record(cs)
+    comp.wait_event(copied)
+    lfmmi_loss_grad(num, den, bufs["emis"][i], bufs["lengths"][i], bufs["grad"], bufs["ws"], bufs["loss"],
+                    bufs["totals"], bufs["status"])
+    done = torch.cuda.Event()
+    done.record(comp)
+    bufs["free"][i] = done
+    out = bufs["out"][i]  # valid once the stream has synchronised, until the call after next
+    out[:5].copy_(bufs["totals"], non_blocking=True)
+    out[5:].copy_(bufs["loss"], non_blocking=True)
+    return out
 
 
 def fb_viterbi(g: Graph, emis, lengths):
