@@ -282,6 +282,8 @@ def run_ours(args, rank, world, local):
     for name, (cnt, tot_ms) in prof.items():
         avg = tot_ms / max(cnt, 1)
         kern[name] = {"launches": cnt, "avg_ms": avg}
+        if name.startswith(("k_fb_", "k_fbc_")):
+            kern[name]["frame_step_us"] = avg * 1e3 / Nw  # per-frame step latency of the recursion
         if name in alg_bytes:
             kern[name]["achieved_gbs"] = alg_bytes[name] / (avg / 1e3) / 1e9
     dom = max((k for k in kern if k in alg_bytes), key=lambda k: kern[k]["avg_ms"] * kern[k]["launches"])
