@@ -313,7 +313,9 @@ __device__ __forceinline__ void pdf_row(const FBArgs &a, uint32_t a_gbuf, uint32
     auto run = [&](uint32_t w) {
         const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
         float acc = 0.f;
-        for (uint32_t i = 0; i < c; ++i) acc += lds_v(a_gbuf + 4 * (q0 + i), 0.f);
+        if (c >= 1) acc = lds_v(a_gbuf + 4 * q0, 0.f);  // ≤ 2 states per pdf branch-free, a loop beyond
+        if (c >= 2) acc += lds_v(a_gbuf + 4 * (q0 + 1), 0.f);
+        for (uint32_t i = 2; i < c; ++i) acc += lds_v(a_gbuf + 4 * (q0 + i), 0.f);
         return sgn * acc;
     };
     if ((D & 1) == 0 && ((uintptr_t)a.post & 7) == 0) {  // pairs of pdfs: one 8-byte map load, one 8-byte store
