@@ -236,7 +236,7 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
         uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
         if (MODE == MODE_FACTORED) {
             float2 a2 = make_float2(0.f, 0.f);  // two accumulators, one packed FFMA2 per arc pair
-#pragma unroll 2
+#pragma unroll 1
             for (int s = 0; s < L2; ++s) {
                 const uint32_t ix = lds_u32(ia);
                 const float2 w2 = lds_f2(wa);
