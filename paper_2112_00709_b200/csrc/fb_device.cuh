@@ -748,6 +748,21 @@ __global__ void __launch_bounds__(MAXT, (MAXT >= 512 ? 1 : (MAXT == 256 ? 2 : 7)
     }
 }
 
+// LF-MMI numerator pass: each (persistent) CTA runs the raw forward AND the raw
+// backward of its sequences back to back, so the pass stays on the SMs it was
+// launched on (a separate backward launch could land on SMs the denominator
+// forward has just released and delay the denominator backward).
+template <int SPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, (MAXT >= 512 ? 1 : (MAXT == 256 ? 2 : 7)))
+    k_fb_num(const FBArgs af, const FBArgs ab) {
+    for (int b = blockIdx.x; b < af.B; b += gridDim.x) {
+        fb_sequence<false, MODE_RAW, SPT, MAXT>(af, b);
+        __syncthreads();  // α, logZ and status of sequence b written (block scope suffices)
+        fb_sequence<true, MODE_RAW, SPT, MAXT>(ab, b);
+        __syncthreads();
+    }
+}
+
 using KFn = void (*)(FBArgs);
 // k_fb<BWD, MODE, spt, MAXT> for a graph's states-per-thread and CTA size;
 // instantiated per (BWD, MODE) in its own translation unit (fb_inst.cu).

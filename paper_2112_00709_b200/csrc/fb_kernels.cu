@@ -432,6 +432,54 @@ static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
     return check_launch("k_fbc launch");
 }
 
+// Numerator forward + backward in one persistent launch (k_fb_num), for CTA
+// sizes 128 / 256; returns FB_ERR_UNSUPPORTED otherwise (the caller then issues
+// the two passes separately).
+using KFnNum = void (*)(FBArgs, FBArgs);
+static KFnNum pick_fb_num(int spt, int T) {
+    if (T == 128) {
+        switch (spt) {
+            case 1: return k_fb_num<1, 128>;
+            case 2: return k_fb_num<2, 128>;
+            case 3: return k_fb_num<3, 128>;
+            case 4: return k_fb_num<4, 128>;
+            case 6: return k_fb_num<6, 128>;
+            default: return k_fb_num<8, 128>;
+        }
+    }
+    if (T == 256) {
+        switch (spt) {
+            case 1: return k_fb_num<1, 256>;
+            case 2: return k_fb_num<2, 256>;
+            case 3: return k_fb_num<3, 256>;
+            case 4: return k_fb_num<4, 256>;
+            case 6: return k_fb_num<6, 256>;
+            default: return k_fb_num<8, 256>;
+        }
+    }
+    return nullptr;
+}
+static fb_status launch_fb_num(const FBArgs &af, const FBArgs &ab, cudaStream_t s, int idle_sms) {
+    const Graph &G = af.g;
+    KFnNum fn = pick_fb_num(G.spt, G.T);
+    if (!fn) return FB_ERR_UNSUPPORTED;
+    const size_t sm = std::max(smem_bytes(G, false, false),
+                               smem_bytes(G, true, true) + pdf_region(POST_PDF_COMPACT, G.pm.U_max, G.D).bytes);
+    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    int grid = af.B;
+    if (idle_sms > 0) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, G.T, sm);
+        grid = std::max(1, std::min(af.B, idle_sms * std::max(occ, 1)));
+    }
+    {
+        ProfScope ps("k_fb_num[G=B]", s);
+        fn<<<grid, G.T, sm, s>>>(af, ab);
+    }
+    return check_launch("k_fb_num launch");
+}
+
 // idle_sms > 0: launch only as many (persistent) CTAs as fit on that many SMs.
 static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw = false, int idle_sms = 0) {
     const Graph &G = a.g;
@@ -616,11 +664,15 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
         FBArgs a = base_args(num, log_emis, lengths, B, N_max);
         a.logZ = zn; a.status = nst;
         if (raw) a.lat64 = num_alpha64; else a.lat = num_alpha;
-        if ((r = launch_fb(false, a, sr->s, raw, confine)) != FB_OK) return r;
         FBArgs c = base_args(num, log_emis, lengths, B, N_max);
         c.status = nst; c.post = gnum; c.post_kind = POST_PDF_COMPACT;
         if (raw) { c.alpha64 = num_alpha64; c.logZ_in = zn; } else c.alpha = num_alpha;
-        if ((r = launch_fb(true, c, sr->s, raw, confine)) != FB_OK) return r;
+        r = (raw && !std::getenv("FBX_NUM_SPLIT")) ? launch_fb_num(a, c, sr->s, confine) : FB_ERR_UNSUPPORTED;
+        if (r == FB_ERR_UNSUPPORTED) {
+            if ((r = launch_fb(false, a, sr->s, raw, confine)) != FB_OK) return r;
+            r = launch_fb(true, c, sr->s, raw, confine);
+        }
+        if (r != FB_OK) return r;
     }
     cudaEventRecord(sr->join, sr->s);
     // denominator backward + fused −Γ_den gradient epilogue: independent of the numerator
