@@ -384,6 +384,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t a_u = sb + (uint32_t)SL.u, a_p = sb + (uint32_t)SL.p, a_part = sb + (uint32_t)SL.part;
     const uint32_t a_wmax = sb + (uint32_t)SL.red, a_wz = a_wmax + 64 * 8, a_flag = a_wmax + 192 * 8;
+    const uint32_t a_cz = a_wmax + 193 * 8;  // [2][2] V: (c, Z) of a frame, computed once by warp 0
     const PdfRegion PR = pdf_region(a.post_kind, G.pm.U_max, a.D);
     unsigned short *ssp = (unsigned short *)(smem_raw + SL.total + PR.ssp);
     uint32_t *pq = (uint32_t *)(smem_raw + SL.total + PR.pq);
@@ -563,12 +564,15 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
             }
         }
     };
-    // γ of the frame whose x and Z (buffers [pp]) were produced one frame ago.
-    auto posterior = [&](int pn, int pp) {
+    // γ of the frame whose x and Z (buffers [pp]) were produced one frame ago;
+    // from_cz: Z was reduced once by warp 0 into cz[pp] (the steady-state step)
+    auto posterior = [&](int pn, int pp, bool from_cz) {
         V Z;
         if (RAW) {  // unnormalised float64 lattices: Eq. (15) with the forward's logZ
             const double z = a.logZ_in[b];
             Z = (z > -INFINITY) ? (V)(z * 1.4426950408889634) : NINF;
+        } else if (from_cz) {
+            Z = lds_v(a_cz + (uint32_t)(2 * pp + 1) * 8, (V)0);
         } else {
             const V m = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane) * 8, (V)0) : NINF;
             const float s = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
@@ -641,6 +645,19 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         __syncthreads();  // u, p, wmax[par], wz[par] of frame n visible
         ++tstep;
         tma_issue(tstep + 1, n_next + dir);  // buffer of step tstep-1 is free now
+        if (!RAW && warp == 0) {  // the frame's normaliser c and posterior Z, reduced once (read after the next barrier)
+            const V cmax = block_max_prev(par);
+            V Zr = (V)0;
+            if (want_post) {
+                const V m = lane < W ? lds_v(a_wz + (uint32_t)(par * 64 + 2 * lane) * 8, (V)0) : NINF;
+                const float s2 = lane < W ? lds_v(a_wz + (uint32_t)(par * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
+                Zr = block_lse_pairs<V>(m, s2);
+            }
+            if (lane == 0) {
+                sts_v(a_cz + (uint32_t)(2 * par) * 8, cmax);
+                sts_v(a_cz + (uint32_t)(2 * par + 1) * 8, Zr);
+            }
+        }
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
         if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T);
         phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
@@ -648,10 +665,10 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         // ---- phase B of frame n_next
         const int pp = par;
         par ^= 1;
-        if (want_post) posterior(n, pp);  // γ_n (its x is in registers, Z in wz[pp])
+        if (want_post) posterior(n, pp, true);  // γ_n (its x is in registers, Z in cz[pp])
         pend_n = n;
         n = n_next;
-        V c = RAW ? (V)0 : block_max_prev(pp);  // lagged normaliser: max of the previous u
+        V c = RAW ? (V)0 : lds_v(a_cz + (uint32_t)(2 * pp) * 8, (V)0);  // lagged normaliser: max of the previous u
         if (c == NINF) c = (V)0;                // no viable state: keep 0̄ everywhere
         scale += (double)c;
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
@@ -687,7 +704,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         __syncthreads();  // wz[par] of the last frame visible; gbuf of pend_n complete
         if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T);
         if (pdf_post) __syncthreads();  // gbuf free again
-        posterior(n, par);
+        posterior(n, par, false);
         if (pdf_post) {
             __syncthreads();
             pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, n, tid, T);

@@ -90,7 +90,8 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sl[a].L > sl[b].L; });
     using Item = std::pair<long long, int>;
     std::priority_queue<Item, std::vector<Item>, std::greater<Item>> heap;
-    for (int w = 0; w < W; ++w) heap.push({0, w});
+    // warp 0 also reduces each frame's normaliser / posterior Z: start it with a little load
+    for (int w = 0; w < W; ++w) heap.push({(w == 0 && W > 1) ? 6 : 0, w});
     std::vector<std::vector<int>> wsl(W);
     for (int q : order) {
         Item it = heap.top();
