@@ -414,3 +414,47 @@ def test_host_entry_pipelined_matches_device_entry(fbx):
         torch.cuda.synchronize()
         ref = np.concatenate([totals.cpu().numpy(), loss.cpu().numpy()])
         assert (out.numpy() == ref).all()
+
+
+@pytest.mark.parametrize("cs", ["2,2", "4,4,1"])
+def test_cluster_status_flags(fbx, cs, monkeypatch):
+    """Fault handling through the cluster kernel: NaN emission, N_b = 0 and N_b > N_max
+    flagged per sequence, the cluster's other sequences unaffected and exact."""
+    import torch
+
+    monkeypatch.setenv("FBX_CLUSTER", cs)
+    w = synth.make_c4(seed=24, B=5, N=30, K=1500, nnz=10000, D=1000, L_range=(10, 20))
+    emis = w.emis.copy()
+    emis[1, 5, :] = np.nan
+    lens = np.array([30, 30, 0, 31, 17], np.int32)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    assert den.info["cluster_C"] > 0
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(emis), dev(lens))
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    assert st[0] == 0 and st[4] == 0
+    assert st[1] & fbx.SEQ_NONFINITE_INPUT
+    assert st[2] & fbx.SEQ_BAD_LENGTH and st[3] & fbx.SEQ_BAD_LENGTH
+    g = grad.cpu().numpy()
+    assert (g[1:4] == 0).all() and np.isfinite(g).all()
+    ref = oracle.lfmmi_batch(synth.compose([w.nums[0], w.nums[4]]), synth.compose([w.den]), emis[[0, 4]],
+                             lens[[0, 4]])
+    assert np.abs(g[[0, 4]] - ref["grad"]).max() <= TOL_GRAD
+    assert totals.cpu().numpy()[4] == 3
+
+
+def test_cluster_determinism_and_batch_independence(fbx, monkeypatch):
+    """k_fbc outputs are bitwise reproducible and an utterance's result does not depend
+    on which sequences share its cluster (no cross-sequence arithmetic)."""
+    monkeypatch.setenv("FBX_CLUSTER", "2,2")
+    w = synth.make_c3(seed=9, B=5, N=40, K=1500, nnz=10000)
+    lens = np.array([40, 31, 40, 7, 22], np.int32)
+    r1 = run_fb(fbx, w.den, w.emis, lens)
+    r2 = run_fb(fbx, w.den, w.emis, lens)
+    assert (r1["post"] == r2["post"]).all() and (r1["logZ"] == r2["logZ"]).all()
+    K = w.den.K
+    perm = np.array([4, 2, 0, 3, 1])  # every utterance gets a different cluster partner
+    r3 = run_fb(fbx, w.den, w.emis[perm].copy(), lens[perm])
+    assert (r3["post"].reshape(5, 40, K) == r1["post"].reshape(5, 40, K)[perm]).all()
+    assert (r3["logZ"] == r1["logZ"][perm]).all()
