@@ -438,18 +438,30 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                     sts_v(x + 8, zs);
                 }
             }
-        } else if (lane < S) {
-            const int s = lane;
+        } else {
+            // S = 4: lane l folds the (warp, sequence) entries w ≡ l/4 (mod 8), s = l % 4, then
+            // three xor shuffles (4, 8, 16) combine the lanes of one sequence
+            const int s = lane & 3;
             float mx = NEG_INF, zm = NEG_INF, zs = 0.f;
-            for (int w = 0; w < W; ++w) {
+            for (int w = lane >> 2; w < W; w += 8) {
                 const uint32_t r = a_red + (uint32_t)((w * S + s) * kCX) * 4;
                 mx = fmaxf(mx, lds_v(r, 0.f));
                 if (want_post) lse2(zm, zs, lds_v(r + 4, 0.f), lds_v(r + 8, 0.f));
             }
-            const uint32_t x = a_x(t, cr, s);
-            sts_v(x, mx);
-            sts_v(x + 4, zm);
-            sts_v(x + 8, zs);
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (want_post) {
+                    const float m2 = __shfl_xor_sync(0xffffffffu, zm, o), s2 = __shfl_xor_sync(0xffffffffu, zs, o);
+                    lse2(zm, zs, m2, s2);
+                }
+            }
+            if (lane < S) {
+                const uint32_t x = a_x(t, cr, s);
+                sts_v(x, mx);
+                sts_v(x + 4, zm);
+                sts_v(x + 8, zs);
+            }
         }
         fence_async_smem();
         __syncwarp();
