@@ -458,3 +458,50 @@ def test_cluster_determinism_and_batch_independence(fbx, monkeypatch):
     r3 = run_fb(fbx, w.den, w.emis[perm].copy(), lens[perm])
     assert (r3["post"].reshape(5, 40, K) == r1["post"].reshape(5, 40, K)[perm]).all()
     assert (r3["logZ"] == r1["logZ"][perm]).all()
+
+
+@pytest.mark.slow
+def test_c5_pool_full_size_sampled(fbx):
+    """configs[4] (C5): the bench's c5-weak batch — 128 utterances of the 1024-utterance pool,
+    N_b log-normal in [50, 700] — through lfmmi_loss_grad; the oracle recomputes sampled
+    utterances (the longest, the shortest, one in between) one by one."""
+    import torch
+    import bench
+
+    w = bench.make_batch(0, 1, "c5-weak")
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(w.emis), dev(w.lengths))
+    torch.cuda.synchronize()
+    st = st.cpu().numpy()
+    assert (st == 0).all()
+    g = grad.cpu().numpy()
+    L = w.lengths
+    for b in (int(np.argmax(L)), int(np.argmin(L)), int(np.argsort(L)[len(L) // 2])):
+        ref = oracle.lfmmi_batch(synth.compose([w.nums[b]]), synth.compose([w.den]), w.emis[b:b + 1], L[b:b + 1])
+        assert abs(loss.cpu().numpy()[b] - ref["loss"][0]) <= TOL_LOGZ * max(1, abs(ref["logZ_den"][0]))
+        assert np.abs(g[b, : L[b]] - ref["grad"][0, : L[b]]).max() <= TOL_GRAD
+        assert (g[b, L[b]:] == 0).all()
+    assert np.abs(g.sum(-1)).max() <= 1e-4
+
+
+@pytest.mark.slow
+def test_n2_full_size_sampled(fbx):
+    """N2 at the paper's Table 1 size (B = 128, N = 700, den 3022 states / 50,984 arcs, cluster
+    kernel) in the bench's launch configuration; sampled utterances against the oracle."""
+    import torch
+
+    w = synth.make_paper_shape(seed=6)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    assert den.info["cluster_C"] > 0
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(w.emis), dev(w.lengths))
+    torch.cuda.synchronize()
+    assert (st.cpu().numpy() == 0).all()
+    g = grad.cpu().numpy()
+    for b in (0, 127):
+        ref = oracle.lfmmi_batch(synth.compose([w.nums[b]]), synth.compose([w.den]), w.emis[b:b + 1],
+                                 w.lengths[b:b + 1])
+        assert abs(loss.cpu().numpy()[b] - ref["loss"][0]) <= TOL_LOGZ * max(1, abs(ref["logZ_den"][0]))
+        assert np.abs(g[b] - ref["grad"][0]).max() <= TOL_GRAD
+    assert np.abs(g.sum(-1)).max() <= 1e-4
