@@ -262,6 +262,7 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
                 sm = (x > m) ? fmaf(sm, e, 1.f) : sm + e;
                 m = hi;
             };
+#pragma unroll 1
             for (int s = 0; s < L2; ++s) {
                 const uint32_t ix = lds_u32(ia);
                 const float2 w2 = lds_f2(wa);
