@@ -758,9 +758,17 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 // Sequences b = blockIdx.x, blockIdx.x + gridDim.x, …  (gridDim.x = B normally;
 // fewer, persistent CTAs confine the numerator pass of lfmmi_loss_grad to the
 // SMs the denominator leaves idle).
+// Work item of CTA c in round r when items are dealt serpentine over g CTAs.
+__device__ __forceinline__ int serpentine(int r, int c, int g) { return r * g + ((r & 1) ? g - 1 - c : c); }
+
 template <bool BWD, int MODEX, int SPT, int MAXT>
 __global__ void __launch_bounds__(MAXT, (MAXT >= 512 ? 1 : (MAXT == 256 ? 2 : 7))) k_fb(const FBArgs a) {
-    for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+    for (int r = 0;; ++r) {
+        // per-sequence graphs: members in descending arc count, dealt serpentine
+        // (round r runs forward or backward over the CTAs) so per-CTA loads balance
+        const int i = serpentine(r, (int)blockIdx.x, (int)gridDim.x);
+        if (i >= a.B) break;
+        const int b = a.g.G == a.B ? a.g.morder[i] : i;
         fb_sequence<BWD, MODEX, SPT, MAXT>(a, b);
         __syncthreads();  // shared memory is reused by the next sequence
     }
@@ -773,7 +781,10 @@ __global__ void __launch_bounds__(MAXT, (MAXT >= 512 ? 1 : (MAXT == 256 ? 2 : 7)
 template <int SPT, int MAXT>
 __global__ void __launch_bounds__(MAXT, (MAXT >= 512 ? 1 : (MAXT == 256 ? 2 : 7)))
     k_fb_num(const FBArgs af, const FBArgs ab) {
-    for (int b = blockIdx.x; b < af.B; b += gridDim.x) {
+    for (int r = 0;; ++r) {
+        const int i = serpentine(r, (int)blockIdx.x, (int)gridDim.x);
+        if (i >= af.B) break;
+        const int b = af.g.morder[i];  // heaviest numerator graphs first (G == B), dealt serpentine
         fb_sequence<false, MODE_RAW, SPT, MAXT>(af, b);
         __syncthreads();  // α, logZ and status of sequence b written (block scope suffices)
         fb_sequence<true, MODE_RAW, SPT, MAXT>(ab, b);

@@ -713,6 +713,12 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     std::vector<int> soff(state_offsets, state_offsets + G + 1);
     size_t o_soff = pk.put(soff), o_pdf = pk.put(pdf), o_i2 = pk.put(init2), o_f2 = pk.put(final2);
     size_t o_df = pk.put(dist_fin), o_ds = pk.put(dist_start);
+    std::vector<int> morder(G);
+    std::iota(morder.begin(), morder.end(), 0);
+    std::stable_sort(morder.begin(), morder.end(), [&](int x, int y) {
+        return row_ptr[state_offsets[x + 1]] - row_ptr[state_offsets[x]] > row_ptr[state_offsets[y + 1]] - row_ptr[state_offsets[y]];
+    });
+    size_t o_mo = pk.put(morder);
     std::vector<float> init_nat(log_init, log_init + K_tot), final_nat(log_final, log_final + K_tot);
     size_t o_in = pk.put(init_nat), o_fn = pk.put(final_nat);
     struct SO { size_t rec, rb, ro, wo, wn; };
@@ -775,6 +781,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.final2 = (const float *)P(o_f2);
     gr.dist_fin = (const int *)P(o_df);
     gr.dist_start = (const int *)P(o_ds);
+    gr.morder = (const int *)P(o_mo);
     gr.init_nat = (const float *)P(o_in);
     gr.final_nat = (const float *)P(o_fn);
     auto set_sched = [&](Sched &d, const SO &o) {

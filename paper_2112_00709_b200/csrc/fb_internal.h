@@ -134,6 +134,7 @@ struct Graph {
     const float *final_nat = nullptr; // [K_tot] ω (natural log, as given)
     const int *dist_fin = nullptr;    // [K_tot] min #transitions to a final state (INT_MAX/2 if none)
     const int *dist_start = nullptr;  // [K_tot] min #transitions from an initial state
+    const int *morder = nullptr;      // [G] members by descending arc count (persistent CTAs take the heavy ones first)
     Sched fwd, bwd;
     Sched vit;        // forward (in-arc) schedule with natural-log weights for fb_viterbi
     int vit_ok = 0;   // the Viterbi schedule fits shared memory
