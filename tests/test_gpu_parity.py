@@ -505,3 +505,23 @@ def test_n2_full_size_sampled(fbx):
         assert abs(loss.cpu().numpy()[b] - ref["loss"][0]) <= TOL_LOGZ * max(1, abs(ref["logZ_den"][0]))
         assert np.abs(g[b] - ref["grad"][0]).max() <= TOL_GRAD
     assert np.abs(g.sum(-1)).max() <= 1e-4
+
+
+def test_lfmmi_multiwave_longest_first(fbx):
+    """B > #SMs (the den recursion runs in several waves, the numerator has no idle SMs):
+    ragged lengths through lfmmi_loss_grad against the oracle, utterance by utterance."""
+    import torch
+
+    B = 200
+    w = synth.make_c4(seed=25, B=B, N=40, K=700, nnz=4000, D=500, L_range=(5, 12))
+    rng = np.random.default_rng(25)
+    lens = rng.integers(14, 41, B).astype(np.int32)
+    num = fbx.Graph.from_host(synth.compose(w.nums))
+    den = fbx.Graph.from_host(w.den)
+    loss, totals, st, grad = fbx.lfmmi_loss_grad(num, den, dev(w.emis), dev(lens))
+    torch.cuda.synchronize()
+    assert (st.cpu().numpy() == 0).all()
+    ref = oracle.lfmmi_batch(synth.compose(w.nums), synth.compose([w.den]), w.emis, lens)
+    assert np.abs(grad.cpu().numpy() - ref["grad"]).max() <= TOL_GRAD
+    err = np.abs(loss.cpu().numpy() - ref["loss"]) / np.maximum(1, np.abs(ref["logZ_den"]))
+    assert err.max() <= TOL_LOGZ
