@@ -185,13 +185,8 @@ struct FBArgs {
     // backward epilogue
     const float *alpha; // α̂ from the forward (natural log), may be null
     int post_kind;
-    float *post;        // state / dense pdf / compact pdf / grad
-    // lfmmi gradient (POST_GRAD): Γ_num compact and the numerator pdf map
-    const float *gnum;
-    const int *num_slot_off;
-    const int *num_pdf_slot; // [B*D]
-    int num_U_max;           // largest numerator slot count (gnbuf size)
-    int tma;                 // stage φ rows in shared memory with TMA bulk copies
+    float *post;        // state / dense pdf / compact pdf / grad (−Γ_den; k_add_num adds Γ_num)
+    int tma;            // stage φ rows in shared memory with TMA bulk copies
     // MODE_RAW (lfmmi numerator): float64 log2 lattices, posteriors normalised by logZ_in
     double *lat64;
     const double *alpha64;
