@@ -291,7 +291,7 @@ def run_ours(args, rank, world, local):
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(dom)
+            traffic = json.load(f).get(args.workload, {}).get(dom)
     achieved = kern.get(dom, {}).get("achieved_gbs")
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "peak_source": peak_src,

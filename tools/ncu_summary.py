@@ -1,5 +1,5 @@
 """Summarise an ncu --set full report: per-kernel duration, DRAM bytes, throughput,
-IPC, smem wavefronts.  Writes profiles/ncu_traffic.json (dram bytes per launch of
+IPC, smem wavefronts, issue-active %, MUFU (xu pipe) and FMA pipe utilisation.  Writes profiles/ncu_traffic.json (dram bytes per launch of
 each kernel name, averaged) and prints a table."""
 import csv
 import io
@@ -16,9 +16,10 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[0]
 H = {h: i for i, h in enumerate(hdr)}
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
-        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__inst_executed_pipe_xu.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size"]
 units = rows[1]
 SCALE = {"": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1, "nsecond": 1,
@@ -53,11 +54,13 @@ for k, lst in agg.items():
     dur_ms = avg["gpu__time_duration.sum"] / 1e6 if "gpu__time_duration.sum" in avg else None
     by = avg.get("dram__bytes_read.sum", 0) + avg.get("dram__bytes_write.sum", 0)
     print(f"{k:36s} n={len(lst)} dur={dur_ms:.3f}ms dram={by/1e9:.3f}GB ({by/1e9/(dur_ms/1e3):.0f} GB/s) "
-          f"dram%={avg.get('dram__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} "
+          f"dram%={avg.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} "
           f"sm%={avg.get('sm__throughput.avg.pct_of_peak_sustained_elapsed', 0):.1f} "
           f"inst={avg.get('smsp__inst_executed.sum', 0)/1e6:.0f}M smem_wf={avg.get('l1tex__data_pipe_lsu_wavefronts_mem_shared.sum', 0)/1e6:.0f}M "
           f"conf={avg.get('l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 0)/1e6:.0f}M "
-          f"xu={avg.get('sm__inst_executed_pipe_xu.sum', 0)/1e6:.0f}M regs={avg.get('launch__registers_per_thread', 0):.0f}")
+          f"issue%={avg.get('smsp__issue_active.avg.pct_of_peak_sustained_active', 0):.1f} "
+          f"mufu%={avg.get('sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active', 0):.1f} "
+          f"fma%={avg.get('sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active', 0):.1f} regs={avg.get('launch__registers_per_thread', 0):.0f}")
 if out_json:
     names = {}
     for k in summary:
