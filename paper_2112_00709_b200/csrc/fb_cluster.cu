@@ -116,10 +116,12 @@ struct VS<4> {
 
 // Phase A over this warp's slices (Sched layout, fb_internal.h) with S-float
 // gathered elements: lane l reduces one row segment for all S sequences.
+// add: accumulate into the part row instead of storing (split schedules).
 // NOP: the gathered array is u itself (log2) and each element is exponentiated
 // on the fly (one MUFU ex2 per sequence-arc) — used when p = 2^u does not fit.
 template <int S, bool NOP>
-__device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uint32_t a_p, uint32_t a_part) {
+__device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uint32_t a_p, uint32_t a_part,
+                                            bool add) {
     for (int q = 0; q < nsl; ++q) {
         const uint32_t h = lds_u32(cur + lane * 4);
         const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
@@ -154,7 +156,16 @@ __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uin
 #pragma unroll
             for (int i = 0; i < S; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
         }
-        if (row >= 0) VS<S>::st(a_part + (uint32_t)row * (S * 4), acc);
+        if (row >= 0) {
+            const uint32_t pa = a_part + (uint32_t)row * (S * 4);
+            if (add) {  // split schedules: the row's other pass wrote (or phase B zeroed) it
+                float o[S];
+                VS<S>::ld(pa, o);
+#pragma unroll
+                for (int i = 0; i < S; ++i) acc[i] += o[i];
+            }
+            VS<S>::st(pa, acc);
+        }
         cur += 128 + (uint32_t)L2 * 384;
     }
 }
@@ -268,10 +279,15 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 
     // ---- schedule and pdf map → shared memory; mbarriers
     {
-        const uint4 *src = (const uint4 *)(SC.rec + SC.rec_off[cr]);
-        uint4 *dst = (uint4 *)(smem_raw + L.rec);
-        const int n16 = SC.rec_bytes[cr] >> 4;
-        for (int x = tid; x < n16; x += T) dst[x] = src[x];
+        const int m0 = P.split ? 2 * cr : cr;  // split: members 2c, 2c+1 back to back
+        for (int m = m0; m <= (P.split ? m0 + 1 : m0); ++m) {
+            const uint4 *src = (const uint4 *)(SC.rec + SC.rec_off[m]);
+            uint4 *dst = (uint4 *)(smem_raw + L.rec + (m > m0 ? SC.rec_bytes[m0] : 0));
+            const int n16 = SC.rec_bytes[m] >> 4;
+            for (int x = tid; x < n16; x += T) dst[x] = src[x];
+        }
+        if (P.split)  // both passes accumulate: part rows start at 0 and phase B re-zeroes them
+            for (int x = tid; x < Kc * S; x += T) sts_v(a_part + 4u * (uint32_t)x, 0.f);
     }
     if (pdf_post)
         for (int d = d_lo + tid; d < d_hi; d += T) sts_i(a_pq + 4u * (uint32_t)(d - d_lo), (int)P.pq[d]);
@@ -537,14 +553,20 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     }
 
     // ---- frames 1 … Tmax−1 (+ one flush step t = Tmax for the last posterior rows)
-    const int nsl = SC.warp_nsl[cr * W + warp];
-    const uint32_t mysl = a_rec + (uint32_t)SC.warp_off[cr * W + warp];
+    const int split = P.split;
+    const int mr = split ? 2 * cr + 1 : cr;  // remote-source (or whole) member
+    const int nsl = SC.warp_nsl[mr * W + warp];
+    const uint32_t mysl = a_rec + (uint32_t)(split ? SC.rec_bytes[2 * cr] : 0) + (uint32_t)SC.warp_off[mr * W + warp];
+    const int nsl_loc = split ? SC.warp_nsl[2 * cr * W + warp] : 0;
+    const uint32_t mysl_loc = a_rec + (uint32_t)(split ? SC.warp_off[2 * cr * W + warp] : 0);
     const int own0 = k0 * S, own1 = (k0 + Kc) * S;  // this part's element range of u / p
     for (int t = 1; t <= Tmax; ++t) {
         const bool last = t == Tmax;
         if (!last) {
             if (want_post) load_alpha(t);
             emis_issue(t + 1);
+            // split: this part's own-source arcs while the other parts' rows are in flight
+            if (split) phase_a_vec<S, NOP>(mysl_loc, nsl_loc, lane, NOP ? a_u(t - 1) : a_p, a_part, true);
         }
         mbar_wait_sleep(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
         const uint32_t up = a_u(t - 1);
@@ -600,7 +622,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 }
             }
         }
-        if (!last) phase_a_vec<S, NOP>(mysl, nsl, lane, NOP ? up : a_p, a_part);
+        if (!last) phase_a_vec<S, NOP>(mysl, nsl, lane, NOP ? up : a_p, a_part, split);
         cpa_wait1();
         __syncthreads();  // part rows, γ rows, step-t emissions complete
         // pdf-level rows of frame t−1 for this part's pdf range (ascending states, ledger L9)
@@ -640,6 +662,10 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             const int j = tid + k * T;
             float acc[S];
             VS<S>::ld(a_part + (uint32_t)(min(j, Kc - 1) * S) * 4, acc);
+            if (split && j < Kc) {
+                const float z[S] = {};
+                VS<S>::st(a_part + (uint32_t)(j * S) * 4, z);
+            }
             bool bad = false;
 #pragma unroll
             for (int s = 0; s < S; ++s) {

@@ -323,7 +323,7 @@ bool bad(float x) { return std::isnan(x) || (std::isinf(x) && x > 0); }
 
 // Host image of a CPlan (fb_internal.h).
 struct HostCPlan {
-    int C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0, emis16 = 0, nop = 0;
+    int C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0, emis16 = 0, nop = 0, split = 0;
     std::vector<int> part_off, pdf_lo, perm, ipdf, idf, ids;
     std::vector<float> ii2, if2;
     std::vector<unsigned> pq;
@@ -348,6 +348,11 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
     const int W = T / 32;
     cp = HostCPlan();
     cp.C = C; cp.S = S; cp.T = T; cp.nop = nop;
+    // local/remote split of phase A around the exchange wait: measured faster for the
+    // no-p (4,4) paper-shape plan (N2 fwd 5.36 → 5.12 ms, bwd 8.72 → 8.36 ms), slower
+    // for (2,2) on C3/C4 (6.52 → 6.94 ms); FBX_CLUSTER_SPLIT=0|1 overrides
+    cp.split = nop ? 1 : 0;
+    if (const char *e = std::getenv("FBX_CLUSTER_SPLIT")) cp.split = std::atoi(e) != 0;
     std::vector<double> cost(D, 0.0);
     for (int k = 0; k < K; ++k)
         cost[pdf[k]] += (in.ptr[k + 1] - in.ptr[k]) + (out.ptr[k + 1] - out.ptr[k]) + 8.0;
@@ -438,26 +443,37 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
         const RowLists &rl = dir ? out : in;
         HostSched &hs = dir ? cp.hb : cp.hf;
         for (int c = 0; c < C; ++c) {
-            RowLists pl;
             const int Kc = cp.part_off[c + 1] - cp.part_off[c];
-            pl.ptr.assign(Kc + 1, 0);
-            for (int r = 0; r < Kc; ++r) {
-                const int o = cp.perm[cp.part_off[c] + r];
-                if (o >= 0)
-                    for (int a = rl.ptr[o]; a < rl.ptr[o + 1]; ++a) {
-                        pl.other.push_back(inv[rl.other[a]]);
-                        pl.w.push_back(rl.w[a]);
-                    }
-                pl.ptr[r + 1] = (int)pl.other.size();
+            // split: member 2c = arcs from this part's own states (run before the
+            // exchange wait), member 2c+1 = arcs from the other parts
+            for (int pass = 0; pass < (cp.split ? 2 : 1); ++pass) {
+                RowLists pl;
+                pl.ptr.assign(Kc + 1, 0);
+                for (int r = 0; r < Kc; ++r) {
+                    const int o = cp.perm[cp.part_off[c] + r];
+                    if (o >= 0)
+                        for (int a = rl.ptr[o]; a < rl.ptr[o + 1]; ++a) {
+                            const int si = inv[rl.other[a]];
+                            const bool local = si >= cp.part_off[c] && si < cp.part_off[c + 1];
+                            if (cp.split && local != (pass == 0)) continue;
+                            pl.other.push_back(si);
+                            pl.w.push_back(rl.w[a]);
+                        }
+                    pl.ptr[r + 1] = (int)pl.other.size();
+                }
+                if (!build_member_sched(pl, Kc, T, MODE_FACTORED, 4 * S, Lmax, hs, true)) return false;
             }
-            if (!build_member_sched(pl, Kc, T, MODE_FACTORED, 4 * S, Lmax, hs, true)) return false;
+        }
+        if (cp.split) {  // both members of a part sit back to back in shared memory
+            hs.bytes_max = 0;
+            for (int c = 0; c < C; ++c) hs.bytes_max = std::max(hs.bytes_max, hs.rec_bytes[2 * c] + hs.rec_bytes[2 * c + 1]);
         }
     }
     cp.smem_fwd = cl_layout(cp.hf.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, false, nop).total;
     cp.smem_bwd = cl_layout(cp.hb.bytes_max, Ki, cp.Kc_max, cp.Dc_max, S, C, W, true, nop).total;
     if (std::getenv("FBX_CLUSTER_DEBUG"))
-        std::fprintf(stderr, "cluster plan C=%d S=%d nop=%d T=%d spt=%d K_int=%d Kc_max=%d rec_fwd=%d rec_bwd=%d smem_fwd=%zu smem_bwd=%zu\n",
-                     C, S, (int)nop, T, cp.spt, cp.K_int, cp.Kc_max, cp.hf.bytes_max, cp.hb.bytes_max, cp.smem_fwd,
+        std::fprintf(stderr, "cluster plan C=%d S=%d nop=%d split=%d T=%d spt=%d K_int=%d Kc_max=%d rec_fwd=%d rec_bwd=%d smem_fwd=%zu smem_bwd=%zu\n",
+                     C, S, (int)nop, cp.split, T, cp.spt, cp.K_int, cp.Kc_max, cp.hf.bytes_max, cp.hb.bytes_max, cp.smem_fwd,
                      cp.smem_bwd);
     return cp.smem_fwd <= (size_t)kSmemLimit && cp.smem_bwd <= (size_t)kSmemLimit;
 }
@@ -743,7 +759,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         o_bp = pk.put(hcp.bptr); o_bs = pk.put(hcp.bsrc); o_bw = pk.put(hcp.bw2);
         CPlan &c = gr.cp;
         c.ok = 1; c.C = hcp.C; c.S = hcp.S; c.T = hcp.T; c.spt = hcp.spt; c.K_int = hcp.K_int;
-        c.Kc_max = hcp.Kc_max; c.Dc_max = hcp.Dc_max; c.emis16 = hcp.emis16; c.nop = hcp.nop;
+        c.Kc_max = hcp.Kc_max; c.Dc_max = hcp.Dc_max; c.emis16 = hcp.emis16; c.nop = hcp.nop; c.split = hcp.split;
         c.fwd.bytes_max = hcp.hf.bytes_max; c.fwd.slots_max = hcp.hf.slots_max;
         c.bwd.bytes_max = hcp.hb.bytes_max; c.bwd.slots_max = hcp.hb.slots_max;
     }

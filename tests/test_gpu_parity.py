@@ -298,11 +298,16 @@ def test_viterbi_c3_den(fbx):
 
 # ------------------------------------------------------------------ cluster-batched kernel (k_fbc)
 
-@pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2", "4,4,1"])
+@pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2", "4,4,1", "4,4,1/split0", "2,2/split1",
+                                "8,4/split1", "8,4,1"])
 def test_cluster_configs_vs_oracle(fbx, cs, monkeypatch):
     """Every (C CTAs, S sequences) cluster configuration of a shared factored
     graph against the oracle: logZ (both directions), α̂ + scale, state and pdf
-    posteriors, ragged lengths (a length-1 sequence, an odd batch)."""
+    posteriors, ragged lengths (a length-1 sequence, an odd batch).  /splitX
+    forces phase A's local/remote arc split on or off (default: on for no-p plans)."""
+    if "/split" in cs:
+        cs, sp = cs.split("/split")
+        monkeypatch.setenv("FBX_CLUSTER_SPLIT", sp)
     monkeypatch.setenv("FBX_CLUSTER", cs)
     w = synth.make_c4(seed=21, B=5, N=48, K=1500, nnz=10000, D=1000, kind="softmax4")
     lens = np.array([48, 1, 30, 48, 17], np.int32)
