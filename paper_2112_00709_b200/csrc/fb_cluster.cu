@@ -582,18 +582,31 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             }
         }
         __syncthreads();  // p complete; this part's extras slot of frame t−1 visible
-        // cluster-wide extras of frame t−1 (fixed part order)
+        // cluster-wide extras of frame t−1: lane q·S + s holds part q's (max, Z pair) of
+        // sequence s; a log2(C)-step xor tree over q (C·S ≤ 32; the combine is commutative,
+        // so every lane — and every CTA of the cluster — gets bitwise the same result),
+        // then lane s broadcasts sequence s
         float cmax[S], Z[S];
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
+        {
             float mx = NEG_INF, zm = NEG_INF, zs = 0.f;
-            for (int q = 0; q < C; ++q) {
-                const uint32_t x = a_x(t - 1, q, s);
-                mx = fmaxf(mx, lds_v(x, 0.f));
-                if (want_post) lse2(zm, zs, lds_v(x + 4, 0.f), lds_v(x + 8, 0.f));
+            if (lane < C * S) {
+                const uint32_t x = a_x(t - 1, lane / S, lane % S);
+                mx = lds_v(x, 0.f);
+                if (want_post) { zm = lds_v(x + 4, 0.f); zs = lds_v(x + 8, 0.f); }
             }
-            cmax[s] = mx;
-            Z[s] = (zm == NEG_INF) ? NEG_INF : zm + lg2(zs);
+            for (int o = S; o < C * S; o <<= 1) {
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (want_post) {
+                    const float m2 = __shfl_xor_sync(0xffffffffu, zm, o), s2 = __shfl_xor_sync(0xffffffffu, zs, o);
+                    lse2(zm, zs, m2, s2);
+                }
+            }
+            const float zl = (zm == NEG_INF) ? NEG_INF : zm + lg2(zs);
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                cmax[s] = __shfl_sync(0xffffffffu, mx, s);
+                Z[s] = want_post ? __shfl_sync(0xffffffffu, zl, s) : NEG_INF;
+            }
         }
         // posteriors of frame t−1 (Eq. (15), normalised by Z_{t−1} = LSE_k(α̂ + β̂))
         if (want_post) {
