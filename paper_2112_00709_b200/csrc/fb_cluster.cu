@@ -641,17 +641,29 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         // pdf-level rows of frame t−1 for this part's pdf range (ascending states, ledger L9)
         if (pdf_post) {
             const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;
+            // one thread per (pdf, sequence) pair (a part owns few pdfs: N2 ~21 × ~36 states),
+            // two interleaved accumulators; consecutive threads write consecutive pdfs
+            const int nd = d_hi - d_lo;
+            for (int pr = tid; pr < nd * S; pr += T) {
+                const int s = pr / nd, d = d_lo + pr % nd;
+                int Nss = Ns[0];
 #pragma unroll
-            for (int s = 0; s < S; ++s) {
-                if (t - 1 >= Ns[s]) continue;
-                float *row = a.post + ((size_t)bs[s] * N_max + frame(s, t - 1)) * D;
-                for (int d = d_lo + tid; d < d_hi; d += T) {
-                    const uint32_t w = lds_u32(a_pq + 4u * (uint32_t)(d - d_lo));
-                    const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
-                    float acc = 0.f;
-                    for (uint32_t i = 0; i < c; ++i) acc += lds_v(a_gbuf + (uint32_t)((q0 + i) * S + s) * 4, 0.f);
-                    row[d] = sgn * acc;
+                for (int q = 1; q < S; ++q) Nss = s == q ? Ns[q] : Nss;
+                if (t - 1 >= Nss) continue;
+                int bss = bs[0];
+#pragma unroll
+                for (int q = 1; q < S; ++q) bss = s == q ? bs[q] : bss;
+                const uint32_t w = lds_u32(a_pq + 4u * (uint32_t)(d - d_lo));
+                const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
+                float acc0 = 0.f, acc1 = 0.f;
+                uint32_t ga = a_gbuf + (uint32_t)(q0 * S + s) * 4;
+                uint32_t i = 0;
+                for (; i + 1 < c; i += 2, ga += 8u * S) {
+                    acc0 += lds_v(ga, 0.f);
+                    acc1 += lds_v(ga + 4u * S, 0.f);
                 }
+                if (i < c) acc0 += lds_v(ga, 0.f);
+                a.post[((size_t)bss * N_max + (BWD ? Nss - 1 - (t - 1) : t - 1)) * D + d] = sgn * (acc0 + acc1);
             }
             if (NOP) __syncthreads();  // γ lives in xbuf, which phase B refills with the next x
         }
