@@ -187,3 +187,17 @@ def test_bank_conflicts_reduced(L):
                     rows += 1
             cur += 128 + L2 * 384
     assert tot / rows < 2.1, tot / rows  # unordered placement averages ~2.6-way
+
+
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_paper_shape_cluster_plan_fits_one_wave(L, split, monkeypatch):
+    """The paper's Table 1 denominator (3022 states, 50,984 arcs, D = 84) does not
+    fit one SM. It must compile to the one-wave (C, S) = (4, 4) cluster plan
+    (32 clusters × 4 CTAs for B = 128), both with phase A split into local and remote
+    arcs (the default for no-p plans) and without it."""
+    monkeypatch.setenv("FBX_CLUSTER_SPLIT", split)
+    w = synth.make_paper_shape(seed=6, B=2)
+    code, h, info = compile_dry(L, w.den)
+    assert code == 0
+    assert (int(info[14]), int(info[15])) == (4, 4)
+    L.fb_graph_destroy(h)
