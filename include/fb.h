@@ -17,8 +17,15 @@
  *    Every compute call is asynchronous on `stream`, never synchronizes the
  *    host and never allocates device memory.
  *  • Synchronous errors: a non-zero fb_status is returned for host-checkable
- *    problems (null pointers, non-positive sizes, G ∉ {1, B}, D mismatch,
- *    workspace too small, unsupported graph sizes); nothing is enqueued then.
+ *    problems (null pointers, non-positive sizes, G ∉ {1, B}, numerator /
+ *    denominator D mismatch, workspace too small, unsupported graph sizes);
+ *    nothing is enqueued then.  The emission width is not an argument: log_emis
+ *    must have exactly the D columns the graph was created with, and buffers
+ *    must have the sizes stated per call — the library cannot check either
+ *    (the Python binding does, and raises ValueError).
+ *  • Threading: entry points are re-entrant; handles are immutable (except the
+ *    diagnostic counters, see fb_graph_counters) and may be used from several
+ *    host threads and streams at once.
  *  • Asynchronous, data-dependent problems never abort a batch: they set
  *    per-sequence bits in seq_status[b] (FB_SEQ_*): empty lattice (logZ = 0̄),
  *    NaN or +∞ in an emission the recursion reads (−∞ is a legal 0̄), and
@@ -130,6 +137,18 @@ fb_status fb_graph_destroy(fb_graph g);
  * cluster-batched kernel (C CTAs per cluster, S sequences per cluster).
  */
 fb_status fb_graph_info(fb_graph g, int64_t *out);
+
+/*
+ * fb_graph_counters — [host] out[2] int64 diagnostic counters of the handle since
+ * creation or the last reset: out[0] = row evaluations of the exp-factorised ⊕
+ * that fell back to the exact max-then-sum because
+ * the factored sum left [2^-80, 2^120] (one-CTA kernel, per row and frame), out[1] =
+ * the same in the cluster kernel (per row, sequence and frame).  Rows of masked
+ * (non-viable) states count too.  reset != 0 zeroes them afterwards.  Synchronous:
+ * waits for all device work (cudaMemcpy).  The counters are the only device state
+ * of a handle that kernels modify (atomic adds); they never influence results.
+ */
+fb_status fb_graph_counters(fb_graph g, int64_t *out, int32_t reset);
 
 /*
  * fb_forward — Eq. (13), the log-domain form of Eq. (2)/(4)

@@ -69,6 +69,27 @@ def _dev(t, dtype, name):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _need(cond: bool, msg: str) -> None:
+    if not cond:
+        raise ValueError(msg)
+
+
+def _check_inputs(g: "Graph", emis, lengths, where: str):
+    """Host-side shape checks the C ABI cannot make (it has no D / length arguments):
+    emis is [B, N_max, g.D] and lengths has B entries; returns (B, N_max, D)."""
+    _need(getattr(emis, "dim", lambda: 0)() == 3, f"{where}: emis must be [B, N_max, D]")
+    B, N_max, D = emis.shape
+    _need(D == g.D, f"{where}: emis has D={D} columns but the graph was built for D={g.D}")
+    _need(lengths.numel() == B, f"{where}: lengths has {lengths.numel()} entries, expected B={B}")
+    _need(g.G in (1, B), f"{where}: graph has G={g.G} members, expected 1 or B={B}")
+    return B, N_max, D
+
+
+def _check_numel(t, n: int, name: str, where: str):
+    if t is not None:
+        _need(t.numel() >= n, f"{where}: {name} has {t.numel()} elements, needs {n}")
+
+
 def _stream():
     import torch
 
@@ -111,6 +132,12 @@ class Graph:
     def handle(self):
         return self._h
 
+    def counters(self, reset: bool = False) -> dict:
+        """fb_graph_counters: exact-fallback row evaluations of the exp-factorised ⊕ (N3)."""
+        out = np.zeros(2, np.int64)
+        _check(lib().fb_graph_counters(self._h, _np_ptr(out), int(bool(reset))), "fb_graph_counters")
+        return {"fallback_rows": int(out[0]), "fallback_rows_cluster": int(out[1])}
+
     def lattice_numel(self, B: int, N_max: int) -> int:
         return B * N_max * self.K_tot if self.G == 1 else N_max * self.K_tot
 
@@ -130,8 +157,10 @@ def fb_forward(g: Graph, emis, lengths, alpha=None, alpha_scale=None, want_alpha
     """Eq. (13) (P:176-178).  Returns (logZ [B] f64, alpha, alpha_scale, status [B] i32)."""
     import torch
 
-    B, N_max, D = emis.shape
+    B, N_max, D = _check_inputs(g, emis, lengths, "fb_forward")
     dev = emis.device
+    _check_numel(alpha, g.lattice_numel(B, N_max), "alpha", "fb_forward")
+    _check_numel(alpha_scale, B * N_max, "alpha_scale", "fb_forward")
     if want_alpha and alpha is None:
         alpha = torch.empty(g.lattice_numel(B, N_max), dtype=torch.float32, device=dev)
     if alpha is not None and alpha_scale is None:
@@ -152,10 +181,12 @@ def fb_backward(g: Graph, emis, lengths, alpha=None, status=None, want_beta=Fals
     Returns (post, logZ_beta, status, beta, beta_scale)."""
     import torch
 
-    B, N_max, D = emis.shape
+    B, N_max, D = _check_inputs(g, emis, lengths, "fb_backward")
     dev = emis.device
     if status is None:
         status = torch.zeros(B, dtype=torch.int32, device=dev)
+    _check_numel(status, B, "status", "fb_backward")
+    _check_numel(alpha, g.lattice_numel(B, N_max), "alpha", "fb_backward")
     beta = beta_scale = None
     if want_beta:
         beta = torch.empty(g.lattice_numel(B, N_max), dtype=torch.float32, device=dev)
@@ -165,6 +196,7 @@ def fb_backward(g: Graph, emis, lengths, alpha=None, status=None, want_beta=Fals
         if alpha is None:
             raise ValueError("posteriors need the forward lattice `alpha`")
         pdf_level = 1 if post == "pdf" else 0
+        _check_numel(post_out, B * N_max * D if pdf_level else g.lattice_numel(B, N_max), "post_out", "fb_backward")
         if post_out is None:
             post_out = torch.empty((B, N_max, D) if pdf_level else (g.lattice_numel(B, N_max),),
                                    dtype=torch.float32, device=dev)
@@ -182,6 +214,11 @@ def fb_posteriors(g: Graph, alpha, beta, lengths, status, B, N_max, pdf_level=Fa
     import torch
 
     dev = alpha.device
+    for t, n, name in ((alpha, g.lattice_numel(B, N_max), "alpha"), (beta, g.lattice_numel(B, N_max), "beta"),
+                       (lengths, B, "lengths"), (status, B, "status"),
+                       (post, B * N_max * g.D if pdf_level else g.lattice_numel(B, N_max), "post")):
+        _check_numel(t, n, name, "fb_posteriors")
+    _need(g.G in (1, B), f"fb_posteriors: graph has G={g.G} members, expected 1 or B={B}")
     if post is None:
         post = torch.empty((B, N_max, g.D) if pdf_level else (g.lattice_numel(B, N_max),), dtype=torch.float32,
                            device=dev)
@@ -200,11 +237,17 @@ def lfmmi_loss_grad(num: Graph, den: Graph, emis, lengths, grad=None, workspace=
     """LF-MMI loss and gradient.  Returns (loss [B] f64, totals [5] f64, status [B], grad)."""
     import torch
 
-    B, N_max, D = emis.shape
+    B, N_max, D = _check_inputs(den, emis, lengths, "lfmmi_loss_grad")
+    _need(num.G == B and num.D == D, f"lfmmi_loss_grad: numerator handle has G={num.G}, D={num.D}; "
+                                     f"expected G=B={B} graphs over D={D} columns")
+    _need(den.G == 1, f"lfmmi_loss_grad: denominator handle has G={den.G}, expected 1")
     dev = emis.device
+    for t, n, name in ((grad, B * N_max * D, "grad"), (loss, B, "loss"), (totals, 5, "totals"), (status, B, "status")):
+        _check_numel(t, n, name, "lfmmi_loss_grad")
     if grad is None:
         grad = torch.empty((B, N_max, D), dtype=torch.float32, device=dev)
     nbytes = workspace_bytes(num, den, B, N_max)
+    _check_numel(workspace, nbytes, "workspace", "lfmmi_loss_grad")
     if workspace is None:
         workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     if loss is None:
@@ -238,6 +281,12 @@ def lfmmi_loss_grad_host(num: Graph, den: Graph, emis_host, lengths_host, bufs: 
 
     B, N_max, D = emis_host.shape
     dev = torch.device("cuda", torch.cuda.current_device())
+    key = (B, N_max, D, dev.index, id(num), id(den))
+    if bufs.get("key") not in (None, key):
+        # a different batch shape or graph pair: wait for the previous calls, then reallocate
+        torch.cuda.current_stream(dev).synchronize()
+        bufs.clear()
+    bufs["key"] = key
     if "emis" not in bufs:
         bufs["emis"] = [torch.empty((B, N_max, D), dtype=torch.float32, device=dev) for _ in range(2)]
         bufs["lengths"] = [torch.empty(B, dtype=torch.int32, device=dev) for _ in range(2)]
@@ -277,7 +326,7 @@ def fb_viterbi(g: Graph, emis, lengths):
     """Tropical-semiring best path.  Returns (score [B] f64, path [B,N_max] i32, status)."""
     import torch
 
-    B, N_max, D = emis.shape
+    B, N_max, D = _check_inputs(g, emis, lengths, "fb_viterbi")
     dev = emis.device
     nbytes = int(lib().fb_viterbi_workspace_bytes(g.handle, B, N_max))
     ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
@@ -299,7 +348,7 @@ def fb_forward_literal(g: Graph, emis, lengths, semiring: int = SEMIRING_LOG):
     phony-state padding, in the log / tropical / probability semiring.  Returns score [B] f64."""
     import torch
 
-    B, N_max, D = emis.shape
+    B, N_max, D = _check_inputs(g, emis, lengths, "fb_forward_literal")
     dev = emis.device
     nbytes = int(lib().fb_literal_workspace_bytes(g.handle, B))
     ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)

@@ -21,6 +21,7 @@ _SIGS = {
     "fb_graph_create": (c_i32, [ctypes.POINTER(c_p), c_i32, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i32, c_i32]),
     "fb_graph_destroy": (c_i32, [c_p]),
     "fb_graph_info": (c_i32, [c_p, c_p]),
+    "fb_graph_counters": (c_i32, [c_p, c_p, c_i32]),
     "fb_forward": (c_i32, [c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p]),
     "fb_backward": (c_i32, [c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_i32, c_p, c_p]),
     "fb_posteriors": (c_i32, [c_p, c_p, c_p, c_p, c_p, c_i32, c_i32, c_i32, c_p, c_p]),

@@ -174,7 +174,8 @@ __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uin
 // (fallback of the factored sum; accurate libm ops; rare).
 template <int S>
 static __device__ __noinline__ float exact_row_c(const int *ptr, const int *src, const float *w2, int row, int s,
-                                                 uint32_t a_uprev) {
+                                                 uint32_t a_uprev, unsigned long long *ctr) {
+    atomicAdd(ctr, 1ull);  // diagnostic: sequence-rows that needed the fallback (fb_graph_counters)
     float m = NEG_INF, sum = 0.f;
     for (int e = ptr[row]; e < ptr[row + 1]; ++e) {
         const float x = lds_v(a_uprev + (uint32_t)(src[e] * S + s) * 4, 0.f) + w2[e];
@@ -286,8 +287,11 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             const int n16 = SC.rec_bytes[m] >> 4;
             for (int x = tid; x < n16; x += T) dst[x] = src[x];
         }
-        if (P.split)  // both passes accumulate: part rows start at 0 and phase B re-zeroes them
-            for (int x = tid; x < Kc * S; x += T) sts_v(a_part + 4u * (uint32_t)x, 0.f);
+        // part rows start at 0 whatever the plan: rows without arcs (states with no in-arcs
+        // in the forward / no out-arcs in the backward) are never written by phase A and
+        // must read as an empty sum (→ exact fallback → 0̄); split plans accumulate both
+        // passes into the rows and phase B re-zeroes them
+        for (int x = tid; x < P.Kc_max * S; x += T) sts_v(a_part + 4u * (uint32_t)x, 0.f);
     }
     if (pdf_post)
         for (int d = d_lo + tid; d < d_hi; d += T) sts_i(a_pq + 4u * (uint32_t)(d - d_lo), (int)P.pq[d]);
@@ -712,7 +716,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 for (int s = 0; s < S; ++s) {
                     if (!(distk[k] <= lim[s]) || (acc[s] >= kTiny && acc[s] <= kHuge)) continue;
                     const float y = exact_row_c<S>(BWD ? P.bptr : P.fptr, BWD ? P.bsrc : P.fsrc, BWD ? P.bw2 : P.fw2,
-                                                   k0 + j, s, up);
+                                                   k0 + j, s, up, G.ctr + 1);
                     const float v = lds_v(eb + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
                     if (!BWD) {
                         h[k][s] = y + fmaf(v, L2E, -c[s]);

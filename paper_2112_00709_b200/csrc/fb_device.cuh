@@ -196,7 +196,9 @@ struct FBArgs {
 // Exact max-then-sum over one row held by g lanes (fallback of factored mode,
 // where weights are stored as e^{T}); `cur` is the slice, `lane` the group
 // leader.  Accurate libm ops; rare.
-static __device__ __noinline__ float exact_row(uint32_t cur, int L2, int g, int lane, uint32_t a_u) {
+static __device__ __noinline__ float exact_row(uint32_t cur, int L2, int g, int lane, uint32_t a_u,
+                                               unsigned long long *ctr) {
+    atomicAdd(ctr, 1ull);  // diagnostic: rows that needed the fallback (fb_graph_counters)
     float m = NEG_INF, sum = 0.f;
     for (int t = 0; t < g; ++t)
         for (int s = 0; s < 2 * L2; ++s) {
@@ -220,7 +222,7 @@ static __device__ __noinline__ float exact_row(uint32_t cur, int L2, int g, int 
 //  exact:    online max-then-sum in V (double) with one ex2 per arc (two chains).
 template <int MODE, class V>
 __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_t a_u, uint32_t a_p,
-                                        uint32_t a_part) {
+                                        uint32_t a_part, unsigned long long *ctr) {
     constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
     constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
     constexpr uint32_t VS = sizeof(V);
@@ -246,7 +248,7 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
             }
             if (row >= 0)
                 sts_v(a_part + (uint32_t)row * VS,
-                      (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(cur, L2, 1 << lg, lane, a_u)));
+                      (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(cur, L2, 1 << lg, lane, a_u, ctr)));
         } else {
             V m0 = ninf<V>(), m1 = ninf<V>();
             float s0 = 0.f, s1 = 0.f;
@@ -439,15 +441,20 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     const bool use_mask = BWD ? G.mask_bwd : G.mask_fwd;
 
     // Owned states j = tid + k*T (k < SPT).  Slots with j ≥ K are inert: their
-    // partial stays 0̄, pdf 0, never stored to HBM.
+    // partial stays 0̄, they are never viable (distance kInert) and never stored to
+    // HBM, and they read the emission column of the member's state 0 — a column the
+    // recursion reads anyway, so the non-finite check (vsum) sees exactly the
+    // columns the graph reads (fb.h; the oracle's rule).
+    constexpr int kInert = 0x3fffffff;
     int pdfk[SPT];   // emission column
     int distk[SPT];  // viability distance
     int posk[SPT];   // position in the slot-ordered γ buffer (pdf-level epilogue)
+    const int pdf0 = G.pdf[s0];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
         const int j = tid + k * T;
-        pdfk[k] = 0;
-        distk[k] = 0;
+        pdfk[k] = pdf0;
+        distk[k] = kInert;
         posk[k] = 0;
         if (j < K) {
             pdfk[k] = G.pdf[s0 + j];
@@ -499,13 +506,18 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const bool in = tid + k * T < K;
-            if (RAW) v[k] = in ? (V)__ldg(a.alpha64 + ro + k * T) : (V)0;
+            // coherent L2 load: in k_fb_num this lattice was written by the same kernel
+            if (RAW) v[k] = in ? (V)__ldcg(a.alpha64 + ro + k * T) : (V)0;
             else v[k] = in ? (V)__ldg(a.alpha + ro + k * T) : (V)0;
         }
     };
     // viable(k, n): forward — a final state is reachable in the N-1-n remaining
     // transitions; backward — the state is reachable from an initial state in n.
-    auto viable = [&](int k, int n) { return !use_mask || (BWD ? (distk[k] <= n) : (distk[k] <= N - 1 - n)); };
+    // (graphs without masked states: every real state has distance 0, so the test
+    // only rejects the inert slots)
+    auto viable = [&](int k, int n) {
+        return use_mask ? (BWD ? (distk[k] <= n) : (distk[k] <= N - 1 - n)) : distk[k] == 0;
+    };
 
     // Ping-pong prefetch buffers (A: even steps, B: odd steps): a buffer is
     // consumed by its frame's phase B and immediately refilled with the frame
@@ -656,7 +668,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         }
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
         if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T);
-        phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part);
+        phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part, G.ctr);
         __syncthreads();
         // ---- phase B of frame n_next
         const int pp = par;

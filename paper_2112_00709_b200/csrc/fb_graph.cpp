@@ -763,6 +763,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         c.fwd.bytes_max = hcp.hf.bytes_max; c.fwd.slots_max = hcp.hf.slots_max;
         c.bwd.bytes_max = hcp.hb.bytes_max; c.bwd.slots_max = hcp.hb.slots_max;
     }
+    size_t o_ctr = pk.put(std::vector<unsigned long long>(2, 0ull));
     size_t o_so = pk.put(slot_off), o_spd = pk.put(slot_pdf), o_ssp = pk.put(slot_sptr),
            o_sst = pk.put(slot_states), o_pds = pk.put(pdf_slot), o_spo = pk.put(slot_pos);
     if (flags & FB_GRAPH_DRY_RUN) {
@@ -820,6 +821,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         c.fptr = (const int *)P(o_fp); c.fsrc = (const int *)P(o_fs); c.fw2 = (const float *)P(o_fw);
         c.bptr = (const int *)P(o_bp); c.bsrc = (const int *)P(o_bs); c.bw2 = (const float *)P(o_bw);
     }
+    gr.ctr = (unsigned long long *)P(o_ctr);
     gr.pm.slot_off = (const int *)P(o_so); gr.pm.slot_pdf = (const int *)P(o_spd);
     gr.pm.slot_sptr = (const int *)P(o_ssp); gr.pm.slot_states = (const int *)P(o_sst);
     gr.pm.pdf_slot = (const int *)P(o_pds);
@@ -849,6 +851,21 @@ extern "C" fb_status fb_graph_info(fb_graph h, int64_t *out) {
                      g.K_max, g.nnz_max, g.fwd.slots_max, g.bwd.slots_max, g.pm.U_max,
                      g.cp.ok ? g.cp.C : 0, g.cp.ok ? g.cp.S : 0};
     std::memcpy(out, v, sizeof v);
+    return FB_OK;
+}
+
+extern "C" fb_status fb_graph_counters(fb_graph h, int64_t *out, int32_t reset) {
+    if (!h || !out || h->g.dry) return FB_ERR_INVALID_ARG;
+    unsigned long long v[2] = {0, 0};
+    cudaError_t e = cudaMemcpy(v, h->g.ctr, sizeof v, cudaMemcpyDeviceToHost);  // synchronizes the device
+    if (e != cudaSuccess) { set_cuda_error("fb_graph_counters", (int)e); return FB_ERR_CUDA; }
+    out[0] = (int64_t)v[0];
+    out[1] = (int64_t)v[1];
+    if (reset) {
+        e = cudaMemset(h->g.ctr, 0, sizeof v);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { set_cuda_error("fb_graph_counters", (int)e); return FB_ERR_CUDA; }
+    }
     return FB_OK;
 }
 

@@ -144,6 +144,11 @@ struct Graph {
     CPlan cp;         // cluster plan (k_fbc); cp.ok == 0: one CTA per sequence (k_fb)
     LitPlan lit;      // the paper's literal block-diagonal strategy (fb_literal.cu, N4)
     int legacy_ok = 1; // the one-CTA-per-sequence kernels fit (else only the cluster path runs)
+    // diagnostic counters in the handle's device block (the only mutable device state of a
+    // handle; atomics): [0] rows of the exp-factorised ⊕ that took the exact max-then-sum
+    // fallback (k_fb, per row evaluation), [1] the same in the cluster kernel k_fbc (per
+    // sequence-row).  Read / reset by fb_graph_counters.
+    unsigned long long *ctr = nullptr;
     void *block = nullptr;
     size_t block_bytes = 0;
     bool dry = false;

@@ -24,6 +24,9 @@
 //
 // All log quantities are carried in base 2 inside the kernels (ex2/lg2 are the
 // native MUFU ops) and converted to natural logs at the HBM boundary.
+#include <map>
+#include <memory>
+
 #include "fb_device.cuh"
 
 namespace fbx {
@@ -374,6 +377,22 @@ static KFn pick(bool bwd, int mode, int spt, int T) {
     return pick_fb<false, MODE_EXACT>(spt, T);
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel) and
+// size: later launches needing no more shared memory skip the driver call.
+static fb_status set_smem(const void *fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t &cur = done[{dev, fn}];
+    if (bytes <= cur) return FB_OK;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    cur = bytes;
+    return FB_OK;
+}
+
 static fb_status check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_cuda_error(what, (int)e); return FB_ERR_CUDA; }
@@ -409,8 +428,8 @@ static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
                  : (P.S == 4 ? pick_fbc<false, 4>(P.spt, P.T, P.nop) : pick_fbc<false, 2>(P.spt, P.T, 0));
     const size_t sm = cl_layout(bwd ? P.bwd.bytes_max : P.fwd.bytes_max, P.K_int, P.Kc_max, P.Dc_max, P.S, P.C,
                                 P.T / 32, bwd, P.nop != 0).total;
-    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    if (fb_status r0 = set_smem((const void *)fn, sm); r0 != FB_OK) return r0;
+    cudaError_t e_launch = cudaSuccess;
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3((unsigned)(P.C * ((a.B + P.S - 1) / P.S)), 1, 1);
@@ -426,9 +445,9 @@ static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
     cfg.numAttrs = 1;
     {
         ProfScope ps(bwd ? "k_fbc_bwd[G=1]" : "k_fbc_fwd[G=1]", s);
-        e = cudaLaunchKernelEx(&cfg, fn, aa);
+        e_launch = cudaLaunchKernelEx(&cfg, fn, aa);
     }
-    if (e != cudaSuccess) { set_cuda_error("k_fbc launch", (int)e); return FB_ERR_CUDA; }
+    if (e_launch != cudaSuccess) { set_cuda_error("k_fbc launch", (int)e_launch); return FB_ERR_CUDA; }
     return check_launch("k_fbc launch");
 }
 
@@ -465,8 +484,7 @@ static fb_status launch_fb_num(const FBArgs &af, const FBArgs &ab, cudaStream_t 
     if (!fn) return FB_ERR_UNSUPPORTED;
     const size_t sm = std::max(smem_bytes(G, false, false),
                                smem_bytes(G, true, true) + pdf_region(POST_PDF_COMPACT, G.pm.U_max, G.D).bytes);
-    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    if (fb_status r0 = set_smem((const void *)fn, sm); r0 != FB_OK) return r0;
     int grid = af.B;
     if (idle_sms > 0) {
         int occ = 0;
@@ -494,8 +512,7 @@ static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw =
              sm + tma_bytes <= (size_t)kSmemLimit && std::getenv("FBX_NO_TMA") == nullptr;
     if (aa.tma) sm += tma_bytes;
     KFn fn = pick(bwd, raw ? (int)MODE_RAW : (aa.tma ? kModeFactoredTma : G.mode), G.spt, G.T);
-    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    if (fb_status r0 = set_smem((const void *)fn, sm); r0 != FB_OK) return r0;
     {
         ProfScope ps(bwd ? (G.G == 1 ? "k_fb_bwd[G=1]" : "k_fb_bwd[G=B]") : (G.G == 1 ? "k_fb_fwd[G=1]" : "k_fb_fwd[G=B]"), s);
         int grid = a.B;
@@ -521,25 +538,49 @@ static FBArgs base_args(fb_graph g, const float *emis, const int *lengths, int B
     return a;
 }
 
-// side stream + events for the concurrent numerator pass of lfmmi_loss_grad
+// Side stream + fork/join events for the concurrent numerator pass of
+// lfmmi_loss_grad, one set per (device, caller stream): calls on different
+// caller streams never share events or side streams, and a per-set mutex is held
+// from the fork record to the join wait, so concurrent host threads calling on
+// the same stream cannot interleave their fork/join pairs either (§8(b):
+// re-entrant entry points, multiple streams allowed).
 struct SideRes {
+    int dev = -1;
+    cudaStream_t caller = nullptr;
     cudaStream_t s = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    std::mutex mu;
 };
 static std::mutex g_side_mu;
-static SideRes g_side[64];
+static std::vector<std::unique_ptr<SideRes>> g_side;
 
-static SideRes *side_res() {
-    int dev = 0;
-    cudaGetDevice(&dev);
+static SideRes *side_res(int dev, cudaStream_t caller, fb_status &err) {
     std::lock_guard<std::mutex> lk(g_side_mu);
-    SideRes &r = g_side[dev & 63];
-    if (!r.s) {
-        cudaStreamCreateWithFlags(&r.s, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming);
+    for (auto &r : g_side)
+        if (r->dev == dev && r->caller == caller) return r.get();
+    auto r = std::make_unique<SideRes>();
+    r->dev = dev;
+    r->caller = caller;
+    cudaError_t e = cudaStreamCreateWithFlags(&r->s, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->fork, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r->join, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        set_cuda_error("lfmmi side stream/events", (int)e);
+        err = FB_ERR_CUDA;
+        return nullptr;
     }
-    return &r;
+    g_side.push_back(std::move(r));
+    return g_side.back().get();
+}
+
+// Per-device SM count (cached: the attribute query is not free on every call).
+static int sm_count(int dev) {
+    static std::mutex mu;
+    static int cache[64] = {0};
+    std::lock_guard<std::mutex> lk(mu);
+    int &c = cache[dev & 63];
+    if (!c) cudaDeviceGetAttribute(&c, cudaDevAttrMultiProcessorCount, dev);
+    return c > 0 ? c : 148;
 }
 
 struct WsLayout {
@@ -607,8 +648,7 @@ extern "C" fb_status fb_posteriors(fb_graph g, const float *alpha, const float *
     const Graph &G = g->g;
     cudaStream_t s = (cudaStream_t)stream;
     size_t sm = (size_t)G.K_max * 4;
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_posteriors, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    if (fb_status r0 = set_smem((const void *)k_posteriors, sm); r0 != FB_OK) return r0;
     {
         ProfScope ps("k_posteriors", s);
         k_posteriors<<<(unsigned)((size_t)B * N_max), 256, sm, s>>>(G, alpha, beta, lengths, seq_status, B, N_max,
@@ -641,8 +681,12 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     double *zn = (double *)(ws + L.zn), *zd = (double *)(ws + L.zd);
     int *nst = (int *)(ws + L.nst);
     cudaStream_t s = (cudaStream_t)stream;
-    SideRes *sr = side_res();
-    fb_status r;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return FB_ERR_CUDA;
+    fb_status r = FB_OK;
+    SideRes *sr = side_res(dev, s, r);
+    if (!sr) return r;
+    std::lock_guard<std::mutex> side_lock(sr->mu);  // fork record … join wait of this call
     // The fork point is recorded before the denominator forward so the numerator
     // pass depends only on prior work; the denominator forward is submitted first:
     // its B CTAs each take a whole SM (registers and shared memory), so the
@@ -655,9 +699,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     }
     cudaStreamWaitEvent(sr->s, sr->fork, 0);
     // SMs the denominator passes leave idle (one den CTA per SM)
-    int dev = 0, nsm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int nsm = sm_count(dev);
     const int idle = nsm - std::min(den_ctas(den->g, base_args(den, log_emis, lengths, B, N_max)), nsm);
     const int confine = idle >= 8 ? idle : 0;
     {
@@ -737,8 +779,7 @@ extern "C" fb_status fb_viterbi(fb_graph g, const float *log_emis, const int32_t
         default: fn = small ? k_viterbi<8, 256> : k_viterbi<8, 1024>; break;
     }
     const size_t sm = viterbi_smem_bytes(G);
-    cudaError_t e = cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) { set_cuda_error("cudaFuncSetAttribute", (int)e); return FB_ERR_CUDA; }
+    if (fb_status r0 = set_smem((const void *)fn, sm); r0 != FB_OK) return r0;
     cudaStream_t s = (cudaStream_t)stream;
     {
         ProfScope ps("k_viterbi", s);
