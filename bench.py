@@ -19,8 +19,12 @@ this host's cores over a bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
+import csv
+import io
 import json
 import os
+import shutil
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,6 +39,8 @@ sys.path.insert(0, ROOT)
 B, N, D, K_DEN, NNZ_DEN = 128, 500, 2000, 3000, 20000
 METRIC = "forward-backward frames×seqs/sec (den graph, B=128) & % HBM roofline @1/2/4/8 GPU"
 WORKLOAD = "C4: LF-MMI loss+grad, den K=3000 nnz=20000 (pdf 3000→2000) + 128 numerator graphs, φ[128,500,2000] fp32 per GPU"
+WORKLOAD_C3 = ("C3: den-only forward + backward with fused state posteriors (fb_forward + fb_backward), K=3000 "
+               "nnz=20000 identity pdf map, φ[128,500,3000] fp32 per GPU")
 WORKLOAD_N2 = ("N2 (paper Table 1 shape, P:445-457): LF-MMI loss+grad, den K=3022 nnz=50984 (pdf →84) + 128 numerator "
                "graphs of ≈454 states, φ[128,700,84] fp32 per GPU")
 
@@ -136,6 +142,12 @@ def make_batch(rank: int, world: int = 1, mode: str = "c4"):
                       for _ in range(w.B)]
             w.emis = synth.emissions(rng, w.B, w.N_max, 84)
         return w
+    if mode == "c3":
+        # C3 (configs[2]): shared den K=3000 / nnz=20000, identity pdf map, φ [128,500,3000]
+        w = synth.make_c3(seed=3, B=B, N=N, K=K_DEN, nnz=NNZ_DEN)
+        if rank:
+            w.emis = synth.emissions(np.random.Generator(np.random.PCG64(3 + 1000 * rank)), B, N, w.D)
+        return w
     if mode != "c4":
         return make_c5_batch(rank, world, mode)
 
@@ -196,6 +208,63 @@ def run_reference(args, rank, world):
 
 # ---------------------------------------------------------------------------- our arm
 
+def ncu_traffic(args, n_launch: int):
+    """DRAM bytes (read + write) of the den kernels of ONE step, measured live by ncu on
+    a child process of this script (same build, same inputs, one lfmmi_loss_grad /
+    fb_forward+fb_backward call): {kernel label: bytes per launch}.  None (with the
+    reason) when ncu is not available or fails; never part of the timed region."""
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    pat = "regex:^k_fbc?$"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum", "--clock-control",
+           "none", "-k", pat, "-c", str(n_launch), "--csv", sys.executable, os.path.abspath(__file__),
+           "--ncu-child", "--workload", args.workload]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    except Exception as e:  # noqa: BLE001
+        return None, f"ncu failed: {e}"
+    rows = [ln for ln in r.stdout.splitlines() if ln.startswith('"')]
+    if not rows:
+        return None, f"ncu rc={r.returncode}: {r.stderr.strip()[-200:]}"
+    per = {}
+    for row in csv.DictReader(io.StringIO("\n".join(rows))):
+        key = (row["ID"], row["Kernel Name"])
+        v = float(row["Metric Value"].replace(",", ""))
+        unit = row.get("Metric Unit", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
+        d = per.setdefault(key, {"bytes": 0.0})
+        if row["Metric Name"].startswith("dram__bytes"):
+            d["bytes"] += v * scale
+    out = {}
+    for (_, kname), d in sorted(per.items(), key=lambda x: int(x[0][0])):
+        label = ("k_fbc" if kname.startswith("k_fbc") else "k_fb") + ("_bwd[G=1]" if "<true" in kname or "<1" in kname
+                                                                      else "_fwd[G=1]")
+        out.setdefault(label, d["bytes"])
+    return out, "ncu (live: child process of this run, --metrics dram__bytes_read.sum,dram__bytes_write.sum)"
+
+
+def ncu_child(args):
+    """One call of the timed step on cuda:0 (profiled by the parent's ncu; no output)."""
+    import torch
+
+    import paper_2112_00709_b200 as fbx
+    from paper_2112_00709_b200 import synth
+
+    torch.cuda.set_device(0)
+    w = make_batch(0, 1, args.workload)
+    den = fbx.Graph.from_host(w.den)
+    emis = torch.from_numpy(w.emis).cuda()
+    lens = torch.from_numpy(w.lengths).cuda()
+    if args.workload == "c3":
+        logZ, alpha, _, st = fbx.fb_forward(den, emis, lens)
+        fbx.fb_backward(den, emis, lens, alpha=alpha, status=st)
+    else:
+        num = fbx.Graph.from_host(synth.compose(w.nums))
+        fbx.lfmmi_loss_grad(num, den, emis, lens)
+    torch.cuda.synchronize()
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -204,6 +273,8 @@ def run_ours(args, rank, world, local):
     from paper_2112_00709_b200 import build, synth
 
     build.build()
+    if world != args.gpus:
+        log(f"[rank {rank}] note: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -211,21 +282,46 @@ def run_ours(args, rank, world, local):
     t0 = time.time()
     w = make_batch(rank, world, args.workload)
     Bw, Nw = w.B, w.N_max
-    num = fbx.Graph.from_host(synth.compose(w.nums))
+    c3 = args.workload == "c3"
+    num = None if c3 else fbx.Graph.from_host(synth.compose(w.nums))
     den = fbx.Graph.from_host(w.den)
-    log(f"[rank {rank}] inputs ready in {time.time() - t0:.1f}s; den {den.info} num K_tot {num.K_tot}")
+    log(f"[rank {rank}] inputs ready in {time.time() - t0:.1f}s; den {den.info} num K_tot {num.K_tot if num else 0}")
     emis = torch.from_numpy(w.emis).to(dev)
     lens = torch.from_numpy(w.lengths).to(dev)
-    grad = torch.empty_like(emis)
-    ws = torch.empty(fbx.workspace_bytes(num, den, Bw, Nw), dtype=torch.uint8, device=dev)
     loss = torch.empty(Bw, dtype=torch.float64, device=dev)
     totals = torch.empty(5, dtype=torch.float64, device=dev)
     status = torch.empty(Bw, dtype=torch.int32, device=dev)
+    if c3:
+        # fb_forward + fb_backward with fused state posteriors (SURVEY §8(d) C3 call sequence)
+        alpha = torch.empty(den.lattice_numel(Bw, Nw), dtype=torch.float32, device=dev)
+        ascale = torch.empty((Bw, Nw), dtype=torch.float64, device=dev)
+        post = torch.empty(den.lattice_numel(Bw, Nw), dtype=torch.float32, device=dev)
+        logZ = torch.empty(Bw, dtype=torch.float64, device=dev)
+        logZb = torch.empty(Bw, dtype=torch.float64, device=dev)
+        L = fbx.lib()
+        sp = fbx._dev  # marshalling helper of the binding (pointer of a CUDA tensor)
 
-    def step():
-        fbx.lfmmi_loss_grad(num, den, emis, lens, grad, ws, loss, totals, status)
-        if world > 1:
-            dist.all_reduce(totals)  # NCCL on the current stream: Σ loss, Σ frames, Σ logZ, n_bad
+        def step():
+            s_ = fbx._stream()
+            fbx._check(L.fb_forward(den.handle, sp(emis, torch.float32, "emis"), sp(lens, torch.int32, "lengths"), Bw,
+                                    Nw, sp(alpha, torch.float32, "alpha"), sp(ascale, torch.float64, "scale"),
+                                    sp(logZ, torch.float64, "logZ"), sp(status, torch.int32, "status"), s_),
+                       "fb_forward")
+            fbx._check(L.fb_backward(den.handle, sp(emis, torch.float32, "emis"), sp(lens, torch.int32, "lengths"),
+                                     Bw, Nw, None, None, sp(logZb, torch.float64, "logZ_beta"),
+                                     sp(alpha, torch.float32, "alpha"), sp(post, torch.float32, "post"), 0,
+                                     sp(status, torch.int32, "status"), s_), "fb_backward")
+            if world > 1:
+                totals[0:1].copy_(logZ.sum().unsqueeze(0))
+                dist.all_reduce(totals)
+    else:
+        grad = torch.empty_like(emis)
+        ws = torch.empty(fbx.workspace_bytes(num, den, Bw, Nw), dtype=torch.uint8, device=dev)
+
+        def step():
+            fbx.lfmmi_loss_grad(num, den, emis, lens, grad, ws, loss, totals, status)
+            if world > 1:
+                dist.all_reduce(totals)  # NCCL on the current stream: Σ loss, Σ frames, Σ logZ, n_bad
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -241,24 +337,21 @@ def run_ours(args, rank, world, local):
     torch.cuda.synchronize()
     fbx.profile_reset()
     fbx.profile_enable(True)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps if flush else 1)]
+    # one event pair per step (device time on the launching stream); without a flush
+    # the steps run back to back and the whole-run time is first start → last end
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
-        if flush:
-            for a_, b_ in evs:
+        for a_, b_ in evs:
+            if flush:
                 scratch.fill_(1.0)
-                a_.record()
-                step()
-                b_.record()
-        else:
-            evs[0][0].record()
-            for _ in range(args.steps):
-                step()
-            evs[0][1].record()
+            a_.record()
+            step()
+            b_.record()
         torch.cuda.synchronize()
     fbx.profile_enable(False)
     prof = fbx.profile_collect()
-    ms = sum(a_.elapsed_time(b_) for a_, b_ in evs)
+    per_step = [a_.elapsed_time(b_) for a_, b_ in evs]
+    ms = sum(per_step) if flush else evs[0][0].elapsed_time(evs[-1][1])
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -276,8 +369,11 @@ def run_ours(args, rank, world, local):
     Dw, Kw = w.D, w.den.K
     alg_bytes = {}  # algorithmic bytes per launch from the rank's true frames
     for kname in ("k_fb", "k_fbc"):
-        alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Dw)  # φ row, α̂ row, grad row
-        alg_bytes[kname + "_fwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw)  # φ row, α̂ row
+        if c3:  # backward: φ row + α̂ row in, γ row out; forward: φ row in, α̂ row out
+            alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Kw)
+        else:   # backward: φ row + α̂ row in, grad row out
+            alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Dw)
+        alg_bytes[kname + "_fwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw)
     kern = {}
     for name, (cnt, tot_ms) in prof.items():
         avg = tot_ms / max(cnt, 1)
@@ -287,14 +383,9 @@ def run_ours(args, rank, world, local):
         if name in alg_bytes:
             kern[name]["achieved_gbs"] = alg_bytes[name] / (avg / 1e3) / 1e9
     dom = max((k for k in kern if k in alg_bytes), key=lambda k: kern[k]["avg_ms"] * kern[k]["launches"])
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        with open(tp) as f:
-            traffic = json.load(f).get(args.workload, {}).get(dom)
     achieved = kern.get(dom, {}).get("achieved_gbs")
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "peak_source": peak_src,
+                "frac": (achieved / hbm) if achieved else None, "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes[dom]}
     step_bytes = alg_bytes["k_fb_bwd[G=1]"] + alg_bytes["k_fb_fwd[G=1]"]
     den_kind = "k_fbc (cluster)" if den.info["cluster_C"] else "k_fb (one CTA per sequence)"
@@ -302,7 +393,7 @@ def run_ours(args, rank, world, local):
 
     # end to end through the public API with host buffers (pinned φ in, totals + loss out)
     e2e = None
-    if rank == 0 or world > 1:
+    if not c3:
         emis_h = torch.from_numpy(w.emis).pin_memory()
         lens_h = torch.from_numpy(w.lengths).pin_memory()
         bufs = {}
@@ -328,12 +419,19 @@ def run_ours(args, rank, world, local):
                "h2d_bytes_per_step": int(emis_h.numel() * 4 + lens_h.numel() * 4),
                "d2h_bytes_per_step": int(out.numel() * 8), "steps": k2}
 
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
         return
+    if not args.no_ncu:
+        tr, src = ncu_traffic(args, 2)
+        roofline["traffic_source"] = src
+        if tr and dom in tr:
+            roofline["traffic"] = tr[dom]
+            roofline["traffic_ratio"] = tr[dom] / alg_bytes[dom]
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and not c3:
         threads = len(os.sched_getaffinity(0))
         n_utts = max(1, min(w.B, 2 * threads))
         rate, dt = cpu_oracle_rate(w, n_utts, threads)
@@ -343,21 +441,39 @@ def run_ours(args, rank, world, local):
     line = {
         "metric": METRIC, "value": value, "unit": "seq-frames/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "step_ms": {"median": statistics.median(per_step), "min": min(per_step), "max": max(per_step),
+                    "note": "per-step CUDA events of rank 0" + ("" if flush else " (steps back to back)")},
         "scaling": "strong" if args.workload == "c5-strong" else "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY §8(d) C4 recipe)",
-        "config": {"workload": {"c4": WORKLOAD, "paper": WORKLOAD_N2}.get(args.workload,
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY §8(d) recipes)",
+        "config": {"workload": {"c4": WORKLOAD, "paper": WORKLOAD_N2, "c3": WORKLOAD_C3}.get(args.workload,
                    f"{args.workload.upper()}: 1024-utterance pool, N_b log-normal median 250 in [50,700], LPT-sharded"),
                    "global_batch": Bw * world if args.workload != "c5-strong" else 1024, "seq_len": Nw,
                    "parallelism": f"dp{world}", "den_kernel": den_kind,
                    "l2": ("L2 flushed between timed steps (256 MB write outside the step events)" if flush else
-                          "inputs larger than L2 (φ 512 MB, grad 512 MB, α̂ 768 MB per step)")},
+                          "inputs larger than L2 (φ ≥ 512 MB, α̂ 768 MB per step)")},
         "hbm_fraction_of_step": (step_bytes / (ms / args.steps / 1e3) / 1e9) / hbm,
         "roofline": roofline, "kernels": kern, "gpu_launches": launches, "clocks": clk.summary(),
         "e2e": e2e, "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 outside a torchrun environment: start N ranks (one process per
+    GPU) with torch.distributed.run on 127.0.0.1 and return their exit code."""
+    if args.impl == "ours":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            log(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
+            return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -367,10 +483,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="c4", choices=["c4", "c5-weak", "c5-strong", "paper"],
-                    help="c4 = the BASELINE metric config (default); c5-* = variable-length 1024-utterance pool; "
-                         "paper = N2, the paper's Table 1 graph shape")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu DRAM-traffic capture (roofline.traffic)")
+    ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--workload", default="c4", choices=["c4", "c3", "c5-weak", "c5-strong", "paper"],
+                    help="c4 = the BASELINE metric config (default); c3 = den fwd+bwd+posteriors call sequence; "
+                         "c5-* = variable-length 1024-utterance pool; paper = N2, the paper's Table 1 graph shape")
     args = ap.parse_args()
+    if args.ncu_child:
+        ncu_child(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)

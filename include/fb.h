@@ -29,7 +29,9 @@
  *  • Asynchronous, data-dependent problems never abort a batch: they set
  *    per-sequence bits in seq_status[b] (FB_SEQ_*): empty lattice (logZ = 0̄),
  *    NaN or +∞ in an emission the recursion reads (−∞ is a legal 0̄), and
- *    N_b ∉ [1, N_max].  Flagged sequences get logZ = −∞; their lattice contents
+ *    N_b ∉ [1, N_max].  Per graph at most one bit is set, in this precedence:
+ *    BAD_LENGTH, else NONFINITE_INPUT, else EMPTY_LATTICE (lfmmi_loss_grad ORs
+ *    the numerator's and the denominator's bits).  Flagged sequences get logZ = −∞; their lattice contents
  *    are unspecified; their posterior / gradient rows are written as 0 and they
  *    are excluded from lfmmi totals.
  *  • Units: every log quantity crossing this boundary is a natural log.
@@ -196,6 +198,21 @@ fb_status fb_backward(fb_graph g, const float *log_emis, const int32_t *lengths,
 fb_status fb_posteriors(fb_graph g, const float *alpha, const float *beta, const int32_t *lengths,
                         const int32_t *seq_status, int32_t B, int32_t N_max, int32_t pdf_level,
                         float *post, void *stream);
+
+/*
+ * fb_gap — the Eq. (1) invariant as a per-sequence diagnostic (SURVEY
+ * §8(a) S5 gap_n, §8(c3)): every frame's Σ_k α_n(k) β_n(k) is the same p(X):
+ *   gap[b] = max_{n < N_b} | ⊕_k (α̂_n(k) ⊗ β̂_n(k)) + C_n + D_n − logZ[b] |
+ * from fb_forward's (alpha, alpha_scale, logZ) and fb_backward's (beta,
+ * beta_scale) of the same inputs; natural log, float64 combine.  A healthy run
+ * has gap ≈ fp32 rounding of the lattices (≲ 1e-5·|logZ|); a frame whose α·β
+ * sum is 0̄ gives +∞.  Sequences with seq_status[b] != 0 (seq_status may be
+ * NULL), N_b ∉ [1, N_max] or logZ = 0̄ get gap = 0.
+ *   gap         [B] float64 out.
+ */
+fb_status fb_gap(fb_graph g, const float *alpha, const double *alpha_scale, const float *beta,
+                 const double *beta_scale, const double *logZ, const int32_t *lengths, const int32_t *seq_status,
+                 int32_t B, int32_t N_max, double *gap, void *stream);
 
 /*
  * fb_workspace_bytes — device workspace lfmmi_loss_grad needs for (num, den, B, N_max):

@@ -24,7 +24,7 @@ import numpy as np
 from ._lib import EXPORTS, lib  # noqa: F401
 
 __all__ = [
-    "FBError", "Graph", "fb_forward", "fb_backward", "fb_posteriors", "lfmmi_loss_grad", "workspace_bytes",
+    "FBError", "Graph", "fb_forward", "fb_backward", "fb_posteriors", "fb_gap", "lfmmi_loss_grad", "workspace_bytes",
     "fb_viterbi", "fb_forward_literal", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
     "SEMIRING_LOG", "SEMIRING_TROPICAL", "SEMIRING_PROB",
     "SEQ_OK", "SEQ_EMPTY_LATTICE", "SEQ_NONFINITE_INPUT", "SEQ_BAD_LENGTH",
@@ -226,6 +226,25 @@ def fb_posteriors(g: Graph, alpha, beta, lengths, status, B, N_max, pdf_level=Fa
                                _dev(lengths, torch.int32, "lengths"), _dev(status, torch.int32, "status"), B, N_max,
                                int(bool(pdf_level)), _dev(post, torch.float32, "post"), _stream()), "fb_posteriors")
     return post
+
+
+def fb_gap(g: Graph, alpha, alpha_scale, beta, beta_scale, logZ, lengths, status=None):
+    """Eq. (1) invariant diagnostic: gap[b] = max_n |⊕_k α̂_n β̂_n + C_n + D_n − logZ_b| (float64 [B])."""
+    import torch
+
+    B, N_max = alpha_scale.shape
+    for t, n, name in ((alpha, g.lattice_numel(B, N_max), "alpha"), (beta, g.lattice_numel(B, N_max), "beta"),
+                       (beta_scale, B * N_max, "beta_scale"), (logZ, B, "logZ"), (lengths, B, "lengths"),
+                       (status, B, "status")):
+        _check_numel(t, n, name, "fb_gap")
+    _need(g.G in (1, B), f"fb_gap: graph has G={g.G} members, expected 1 or B={B}")
+    gap = torch.empty(B, dtype=torch.float64, device=alpha.device)
+    _check(lib().fb_gap(g.handle, _dev(alpha, torch.float32, "alpha"), _dev(alpha_scale, torch.float64, "alpha_scale"),
+                        _dev(beta, torch.float32, "beta"), _dev(beta_scale, torch.float64, "beta_scale"),
+                        _dev(logZ, torch.float64, "logZ"), _dev(lengths, torch.int32, "lengths"),
+                        _dev(status, torch.int32, "status"), B, N_max, _dev(gap, torch.float64, "gap"), _stream()),
+           "fb_gap")
+    return gap
 
 
 def workspace_bytes(num: Graph, den: Graph, B: int, N_max: int) -> int:

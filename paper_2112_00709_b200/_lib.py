@@ -25,6 +25,7 @@ _SIGS = {
     "fb_forward": (c_i32, [c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p]),
     "fb_backward": (c_i32, [c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_i32, c_p, c_p]),
     "fb_posteriors": (c_i32, [c_p, c_p, c_p, c_p, c_p, c_i32, c_i32, c_i32, c_p, c_p]),
+    "fb_gap": (c_i32, [c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_p, c_i32, c_i32, c_p, c_p]),
     "fb_workspace_bytes": (c_sz, [c_p, c_p, c_i32, c_i32]),
     "lfmmi_loss_grad": (c_i32, [c_p, c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "fb_viterbi_workspace_bytes": (c_sz, [c_p, c_i32, c_i32]),

@@ -776,8 +776,8 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         double z = -INFINITY;
         if (Ns[s] > 0) {
             z = (M == -INFINITY) ? -INFINITY : (scale[s] + M + log2(tot)) * kLN2;
-            if (!(vq < INFINITY)) st |= FB_SEQ_NONFINITE_INPUT;
-            if (!(z > -INFINITY)) st |= FB_SEQ_EMPTY_LATTICE;
+            if (!(vq < INFINITY)) st |= FB_SEQ_NONFINITE_INPUT;  // precedence as in fb.h: non-finite, else empty
+            else if (!(z > -INFINITY)) st |= FB_SEQ_EMPTY_LATTICE;
         }
         if (st) z = -INFINITY;
         if (a.logZ) a.logZ[bs[s]] = z;

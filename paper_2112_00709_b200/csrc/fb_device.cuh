@@ -748,8 +748,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
             if (lane == 0) {
                 double z = (M == NINF) ? -INFINITY : (scale + Md + log2(t)) * kLN2;
                 int stt = st;
-                if (lds_i(a_flag) == 1) stt |= FB_SEQ_NONFINITE_INPUT;
-                if (!(z > -INFINITY)) stt |= FB_SEQ_EMPTY_LATTICE;
+                if (lds_i(a_flag) == 1) stt |= FB_SEQ_NONFINITE_INPUT;  // precedence (fb.h): non-finite,
+                else if (!(z > -INFINITY)) stt |= FB_SEQ_EMPTY_LATTICE;  // else empty
                 if (stt) z = -INFINITY;
                 if (a.logZ) a.logZ[b] = z;
                 a.status[b] = stt;

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const 
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
         const int j = tid + k * T;
-        pdfk[k] = j < K ? G.pdf[s0 + j] : 0;
+        pdfk[k] = G.pdf[s0 + (j < K ? j : 0)];  // inert slots read a column the graph reads (status parity)
         sts_v(a_best + (uint32_t)j * 8, NEG_INF_D);
     }
     const float *em = a.emis + (size_t)b * a.N_max * a.D;
@@ -238,8 +238,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const 
         }
         if (lane == 0) {
             int st = 0;
-            if (bad) st |= FB_SEQ_NONFINITE_INPUT;
-            if (best == NEG_INF_D) st |= FB_SEQ_EMPTY_LATTICE;
+            if (bad) st |= FB_SEQ_NONFINITE_INPUT;  // precedence as in fb.h: non-finite, else empty
+            else if (best == NEG_INF_D) st |= FB_SEQ_EMPTY_LATTICE;
             a.score[b] = st ? -INFINITY : best;
             a.status[b] = st;
             int s = st ? -1 : arg;
@@ -303,6 +303,58 @@ __global__ void __launch_bounds__(256) k_posteriors(const Graph G, const float *
             for (int q = pm.slot_sptr[so + sl]; q < pm.slot_sptr[so + sl + 1]; ++q) acc += g[pm.slot_states[q]];
         out[d] = acc;
     }
+}
+
+// ------------------------------------------------------------------ Eq. (1) invariant diagnostic
+
+// One CTA per sequence: gap_b = max_{n<N_b} |Z_n + C_n + D_n − logZ_b| with
+// Z_n = ⊕_k α̂_n(k) ⊗ β̂_n(k) (block log-sum-exp, natural log, float64 combine).
+// By Eq. (1) every frame's α·β sum is the same log Z, so the gap
+// measures the accumulated rounding of the normalised fp32 lattices.
+__global__ void __launch_bounds__(256) k_gap(const Graph G, const float *alpha, const double *ascale,
+                                             const float *beta, const double *bscale, const double *logZ,
+                                             const int *lengths, const int *status, int B, int N_max,
+                                             double *gap) {
+    __shared__ double wz[2 * 8];
+    const int b = blockIdx.x;
+    const int gi = (G.G == 1) ? 0 : b;
+    const int s0 = G.state_off[gi], K = G.state_off[gi + 1] - s0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = blockDim.x >> 5;
+    const int N = lengths[b];
+    if (N < 1 || N > N_max || (status && status[b] != 0) || !(logZ[b] > -INFINITY)) {
+        if (tid == 0) gap[b] = 0.0;  // flagged sequences: no invariant to check (the oracle's convention)
+        return;
+    }
+    const size_t base = (size_t)N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
+    double gmax = 0.0;
+    for (int n = 0; n < N; ++n) {
+        double m = NEG_INF_D;
+        for (int j = tid; j < K; j += blockDim.x)
+            m = fmax(m, (double)__ldg(alpha + base + (size_t)n * K + j) + (double)__ldg(beta + base + (size_t)n * K + j));
+        m = warp_max(m);
+        if (lane == 0) wz[warp] = m;
+        __syncthreads();
+        m = lane < W ? wz[lane] : NEG_INF_D;
+        m = warp_max(m);
+        double s = 0.0;
+        if (m > NEG_INF_D)
+            for (int j = tid; j < K; j += blockDim.x)
+                s += exp((double)__ldg(alpha + base + (size_t)n * K + j) +
+                         (double)__ldg(beta + base + (size_t)n * K + j) - m);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        __syncthreads();
+        if (lane == 0) wz[8 + warp] = s;
+        __syncthreads();
+        s = lane < W ? wz[8 + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double zn = (m > NEG_INF_D) ? m + log(s) + ascale[(size_t)b * N_max + n] + bscale[(size_t)b * N_max + n]
+                                          : NEG_INF_D;
+        gmax = fmax(gmax, (zn > NEG_INF_D) ? fabs(zn - logZ[b]) : INFINITY);
+        __syncthreads();
+    }
+    if (tid == 0) gap[b] = gmax;
 }
 
 // ------------------------------------------------------------------ numerator contribution
@@ -655,6 +707,21 @@ extern "C" fb_status fb_posteriors(fb_graph g, const float *alpha, const float *
                                                                   G.D, pdf_level, post);
     }
     return check_launch("k_posteriors launch");
+}
+
+extern "C" fb_status fb_gap(fb_graph g, const float *alpha, const double *alpha_scale, const float *beta,
+                            const double *beta_scale, const double *logZ, const int32_t *lengths,
+                            const int32_t *seq_status, int32_t B, int32_t N_max, double *gap, void *stream) {
+    if (!g || !alpha || !alpha_scale || !beta || !beta_scale || !logZ || !lengths || !gap || B < 1 || N_max < 1)
+        return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B) || g->g.dry) return FB_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    {
+        ProfScope ps("k_gap", s);
+        k_gap<<<(unsigned)B, 256, 0, s>>>(g->g, alpha, alpha_scale, beta, beta_scale, logZ, lengths, seq_status, B,
+                                          N_max, gap);
+    }
+    return check_launch("k_gap launch");
 }
 
 extern "C" size_t fb_workspace_bytes(fb_graph num, fb_graph den, int32_t B, int32_t N_max) {

@@ -205,6 +205,37 @@ def test_lfmmi_one_state():
     assert (np.abs(r["grad"]) <= 1e-12).all()
 
 
+def test_lfmmi_totals_closed_form_one_state():
+    """All five totals on a batch of 1-state numerators / a 1-state denominator,
+    where every quantity has a closed form (S:351, S:456): logZ_b = Σ_{n<N_b} v_{b,n}
+    + (N_b − 1)·t + π + ω.  Pins totals[2] (Σ logZ_num) and totals[3] (Σ logZ_den)
+    separately — a swap or a dropped term fails — and the exclusion of flagged
+    sequences (NaN emission, bad length) from every total (§8(b))."""
+    rng = np.random.default_rng(31)
+    B, N_max = 6, 9
+    tn = [float(np.float32(x)) for x in rng.uniform(-2, -0.1, B)]
+    pin = [float(np.float32(x)) for x in rng.uniform(-1, 0, B)]
+    td, pid, omd = float(np.float32(-1.3)), float(np.float32(-0.25)), float(np.float32(-0.5))
+    nums = [helpers.one_state(tn[b], pin[b], 0.0) for b in range(B)]
+    den = helpers.one_state(td, pid, omd)
+    emis = rng.uniform(-4, 0, (B, N_max, 1)).astype(np.float32)
+    lens = np.array([9, 1, 5, 9, 3, 10], np.int32)  # b = 5: N_b > N_max
+    emis[3, 7, 0] = np.nan                            # b = 3: non-finite emission read
+    r = oracle.lfmmi_batch(synth.compose(nums), synth.compose([den]), emis, lens)
+    ok = np.array([True, True, True, False, True, False])
+    assert ((r["status"] == 0) == ok).all()
+    e64 = emis.astype(np.float64)
+    zn = np.array([e64[b, : lens[b], 0].sum() + (lens[b] - 1) * tn[b] + pin[b] for b in range(B) if ok[b]])
+    zd = np.array([e64[b, : lens[b], 0].sum() + (lens[b] - 1) * td + pid + omd for b in range(B) if ok[b]])
+    t = r["totals"]
+    assert t[2] == pytest.approx(zn.sum(), abs=1e-11)
+    assert t[3] == pytest.approx(zd.sum(), abs=1e-11)
+    assert t[0] == pytest.approx((zn - zd).sum(), abs=1e-11)
+    assert t[1] == lens[ok].sum() and t[4] == 2
+    assert r["logZ_num"][ok] == pytest.approx(zn, abs=1e-12)
+    assert r["logZ_den"][ok] == pytest.approx(zd, abs=1e-12)
+
+
 def test_lfmmi_shift_one_frame():
     # S:467: shifting one frame's φ row by c leaves ℒ and grad unchanged
     rng = np.random.default_rng(9)
