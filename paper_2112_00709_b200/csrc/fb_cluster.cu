@@ -689,8 +689,8 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int j = tid + k * T;
-            float acc[S];
-            VS<S>::ld(a_part + (uint32_t)(min(j, Kc - 1) * S) * 4, acc);
+            float acc[S] = {};
+            if (j < Kc) VS<S>::ld(a_part + (uint32_t)(j * S) * 4, acc);  // inert slots read nothing (racecheck-clean)
             if (split && j < Kc) {
                 const float z[S] = {};
                 VS<S>::st(a_part + (uint32_t)(j * S) * 4, z);

@@ -249,6 +249,30 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
             if (row >= 0)
                 sts_v(a_part + (uint32_t)row * VS,
                       (V)((acc >= kTiny && acc <= kHuge) ? lg2(acc) : exact_row(cur, L2, 1 << lg, lane, a_u, ctr)));
+        } else if (L2 <= 2) {
+            // ≤ 4 arcs per lane (every slice of an exact-mode schedule with Lmax = 4 unless a
+            // row exceeds 32 lanes × 4 arcs): gather all, then max-then-sum — no online
+            // rescaling chain.  Null slots carry weight −∞ (x = −∞, 2^{x−m} = 0).
+            const uint32_t ix0 = lds_u32(ia);
+            const float2 w0 = lds_f2(wa);
+            const V x0 = lds_v(a_u + (ix0 & 0xFFFFu), (V)0) + (V)w0.x;
+            const V x1 = lds_v(a_u + (ix0 >> 16), (V)0) + (V)w0.y;
+            V x2 = ninf<V>(), x3 = ninf<V>();
+            if (L2 == 2) {
+                const uint32_t ix1 = lds_u32(ia + 128);
+                const float2 w1 = lds_f2(wa + 256);
+                x2 = lds_v(a_u + (ix1 & 0xFFFFu), (V)0) + (V)w1.x;
+                x3 = lds_v(a_u + (ix1 >> 16), (V)0) + (V)w1.y;
+            }
+            V m0 = fmax(fmax(x0, x1), fmax(x2, x3));
+            const V ms = (m0 == ninf<V>()) ? (V)0 : m0;
+            float s0 = (ex2((float)(x0 - ms)) + ex2((float)(x1 - ms))) + (ex2((float)(x2 - ms)) + ex2((float)(x3 - ms)));
+            for (int o = 1; o < (1 << lg); o <<= 1) {
+                V m2 = __shfl_xor_sync(0xffffffffu, m0, o);
+                float s2 = __shfl_xor_sync(0xffffffffu, s0, o);
+                lse_combine(m0, s0, m2, s2);
+            }
+            if (row >= 0) sts_v(a_part + (uint32_t)row * VS, (m0 == ninf<V>()) ? m0 : m0 + (V)lg2(s0));
         } else {
             V m0 = ninf<V>(), m1 = ninf<V>();
             float s0 = 0.f, s1 = 0.f;

@@ -575,7 +575,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     if ((gr.K_max + T - 1) / T > kMaxSPT) return FB_ERR_UNSUPPORTED;
     gr.T = T;
     // longest row segment per lane before a row is split over 2, 4, … lanes
-    int lmax = gr.mode == MODE_FACTORED ? 12 : 4;
+    int lmax = gr.mode == MODE_FACTORED ? 24 : 4;  // factored: 24 measured 2% faster than 12 on C4 (fewer slices)
     if (const char *e = std::getenv("FBX_LMAX")) lmax = std::max(1, std::atoi(e));
     gr.W = T / 32;
     gr.spt = spt;
