@@ -142,6 +142,10 @@ def make_batch(rank: int, world: int = 1, mode: str = "c4"):
                       for _ in range(w.B)]
             w.emis = synth.emissions(rng, w.B, w.N_max, 84)
         return w
+    if mode == "viterbi":
+        return make_batch(rank, world, "c3")
+    if mode == "viterbi-paper":
+        return make_batch(rank, world, "paper")
     if mode == "c3":
         # C3 (configs[2]): shared den K=3000 / nnz=20000, identity pdf map, φ [128,500,3000]
         w = synth.make_c3(seed=3, B=B, N=N, K=K_DEN, nnz=NNZ_DEN)
@@ -283,7 +287,8 @@ def run_ours(args, rank, world, local):
     w = make_batch(rank, world, args.workload)
     Bw, Nw = w.B, w.N_max
     c3 = args.workload == "c3"
-    num = None if c3 else fbx.Graph.from_host(synth.compose(w.nums))
+    vit = args.workload.startswith("viterbi")
+    num = None if (c3 or vit) else fbx.Graph.from_host(synth.compose(w.nums))
     den = fbx.Graph.from_host(w.den)
     log(f"[rank {rank}] inputs ready in {time.time() - t0:.1f}s; den {den.info} num K_tot {num.K_tot if num else 0}")
     emis = torch.from_numpy(w.emis).to(dev)
@@ -291,7 +296,23 @@ def run_ours(args, rank, world, local):
     loss = torch.empty(Bw, dtype=torch.float64, device=dev)
     totals = torch.empty(5, dtype=torch.float64, device=dev)
     status = torch.empty(Bw, dtype=torch.int32, device=dev)
-    if c3:
+    if vit:
+        # N1: tropical-semiring best path (fb_viterbi) over the shared den graph
+        L = fbx.lib()
+        sp = fbx._dev
+        score = torch.empty(Bw, dtype=torch.float64, device=dev)
+        path = torch.empty((Bw, Nw), dtype=torch.int32, device=dev)
+        vws = torch.empty(int(L.fb_viterbi_workspace_bytes(den.handle, Bw, Nw)), dtype=torch.uint8, device=dev)
+
+        def step():
+            fbx._check(L.fb_viterbi(den.handle, sp(emis, torch.float32, "emis"), sp(lens, torch.int32, "lengths"), Bw,
+                                    Nw, sp(score, torch.float64, "score"), sp(path, torch.int32, "path"),
+                                    sp(status, torch.int32, "status"), sp(vws, torch.uint8, "ws"), vws.numel(),
+                                    fbx._stream()), "fb_viterbi")
+            if world > 1:
+                totals[0:1].copy_(score.sum().unsqueeze(0))
+                dist.all_reduce(totals)
+    elif c3:
         # fb_forward + fb_backward with fused state posteriors (SURVEY §8(d) C3 call sequence)
         alpha = torch.empty(den.lattice_numel(Bw, Nw), dtype=torch.float32, device=dev)
         ascale = torch.empty((Bw, Nw), dtype=torch.float64, device=dev)
@@ -368,6 +389,8 @@ def run_ours(args, rank, world, local):
     seq_frames = float(w.lengths.sum())
     Dw, Kw = w.D, w.den.K
     alg_bytes = {}  # algorithmic bytes per launch from the rank's true frames
+    bp_bytes = 2 if w.den.K <= 32767 else 4
+    alg_bytes["k_viterbi"] = seq_frames * (4 * min(Dw, Kw) + bp_bytes * Kw)  # φ row (the columns read) + backpointer row
     for kname in ("k_fb", "k_fbc"):
         if c3:  # backward: φ row + α̂ row in, γ row out; forward: φ row in, α̂ row out
             alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Kw)
@@ -387,13 +410,13 @@ def run_ours(args, rank, world, local):
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes[dom]}
-    step_bytes = alg_bytes["k_fb_bwd[G=1]"] + alg_bytes["k_fb_fwd[G=1]"]
+    step_bytes = alg_bytes["k_viterbi"] if vit else alg_bytes["k_fb_bwd[G=1]"] + alg_bytes["k_fb_fwd[G=1]"]
     den_kind = "k_fbc (cluster)" if den.info["cluster_C"] else "k_fb (one CTA per sequence)"
     launches = sum(c for c, _ in prof.values())
 
     # end to end through the public API with host buffers (pinned φ in, totals + loss out)
     e2e = None
-    if not c3:
+    if not (c3 or vit):
         emis_h = torch.from_numpy(w.emis).pin_memory()
         lens_h = torch.from_numpy(w.lengths).pin_memory()
         bufs = {}
@@ -424,14 +447,14 @@ def run_ours(args, rank, world, local):
         dist.destroy_process_group()
     if rank != 0:
         return
-    if not args.no_ncu:
+    if not args.no_ncu and not vit:
         tr, src = ncu_traffic(args, 2)
         roofline["traffic_source"] = src
         if tr and dom in tr:
             roofline["traffic"] = tr[dom]
             roofline["traffic_ratio"] = tr[dom] / alg_bytes[dom]
     cpu = None
-    if not args.no_cpu_baseline and not c3:
+    if not args.no_cpu_baseline and not (c3 or vit):
         threads = len(os.sched_getaffinity(0))
         n_utts = max(1, min(w.B, 2 * threads))
         rate, dt = cpu_oracle_rate(w, n_utts, threads)
@@ -445,7 +468,10 @@ def run_ours(args, rank, world, local):
                     "note": "per-step CUDA events of rank 0" + ("" if flush else " (steps back to back)")},
         "scaling": "strong" if args.workload == "c5-strong" else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY §8(d) recipes)",
-        "config": {"workload": {"c4": WORKLOAD, "paper": WORKLOAD_N2, "c3": WORKLOAD_C3}.get(args.workload,
+        "config": {"workload": {"c4": WORKLOAD, "paper": WORKLOAD_N2, "c3": WORKLOAD_C3,
+                                "viterbi": "N1: Viterbi (tropical semiring, fb_viterbi) over the C3 den, φ[128,500,3000]",
+                                "viterbi-paper": "N1: Viterbi over the paper's Table 1 den (3022 st / 50,984 arcs, "
+                                                 "schedule streamed from L2), φ[128,700,84]"}.get(args.workload,
                    f"{args.workload.upper()}: 1024-utterance pool, N_b log-normal median 250 in [50,700], LPT-sharded"),
                    "global_batch": Bw * world if args.workload != "c5-strong" else 1024, "seq_len": Nw,
                    "parallelism": f"dp{world}", "den_kernel": den_kind,
@@ -485,7 +511,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu DRAM-traffic capture (roofline.traffic)")
     ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
-    ap.add_argument("--workload", default="c4", choices=["c4", "c3", "c5-weak", "c5-strong", "paper"],
+    ap.add_argument("--workload", default="c4",
+                    choices=["c4", "c3", "c5-weak", "c5-strong", "paper", "viterbi", "viterbi-paper"],
                     help="c4 = the BASELINE metric config (default); c3 = den fwd+bwd+posteriors call sequence; "
                          "c5-* = variable-length 1024-utterance pool; paper = N2, the paper's Table 1 graph shape")
     args = ap.parse_args()

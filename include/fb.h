@@ -246,7 +246,9 @@ fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *log_emis, con
  * score[b] = max over accepting paths of π ⊗ Π v ⊗ Π T ⊗ ω and path[b][n] its
  * state sequence (local state ids; −1 for n ≥ N_b), ties broken by the lowest
  * state index at every argmax.  workspace ≥ fb_viterbi_workspace_bytes(g, B, N_max)
- * holds the int16/int32 backpointer lattice.
+ * holds the int16/int32 backpointer lattice.  One CTA per sequence; a schedule too
+ * large for shared memory (e.g. the paper's 50,984-arc denominator) is streamed
+ * from global memory (L2) each frame.  FB_ERR_UNSUPPORTED only for K_g > 8192.
  */
 size_t fb_viterbi_workspace_bytes(fb_graph g, int32_t B, int32_t N_max);
 fb_status fb_viterbi(fb_graph g, const float *log_emis, const int32_t *lengths, int32_t B, int32_t N_max,

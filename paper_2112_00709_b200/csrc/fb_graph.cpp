@@ -480,8 +480,9 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
 
 }  // namespace
 
-size_t viterbi_smem_bytes(const Graph &g) {
-    return smem_layout(g.vit.bytes_max, g.T * g.spt, true, false).total + fbx_a16((size_t)g.T * g.spt * 4);
+size_t viterbi_smem_bytes(const Graph &g, bool global_sched) {
+    return smem_layout(global_sched ? 0 : g.vit.bytes_max, g.T * g.spt, true, false).total +
+           fbx_a16((size_t)g.T * g.spt * 4);
 }
 
 size_t smem_bytes(const Graph &g, bool backward, bool post) {
@@ -688,7 +689,10 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
     gr.bwd.bytes_max = hb.bytes_max; gr.bwd.slots_max = hb.slots_max;
     gr.vit.bytes_max = hv.bytes_max; gr.vit.slots_max = hv.slots_max;
-    gr.vit_ok = vit_ok && viterbi_smem_bytes(gr) <= (size_t)kSmemLimit;
+    // Viterbi schedules that exceed one SM's shared memory (the paper's 50,984-arc
+    // denominator, N2) stay in global memory and are streamed through L2 each frame
+    gr.vit_ok = vit_ok;
+    gr.vit_global = vit_ok && viterbi_smem_bytes(gr) > (size_t)kSmemLimit;
     if (!gr.vit_ok) hv = HostSched();
     gr.pm.U_tot = slot_off[G];
     // cluster plan (k_fbc) for a shared factored graph: the first (C, S) that fits

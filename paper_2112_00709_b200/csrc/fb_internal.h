@@ -139,7 +139,8 @@ struct Graph {
     const int *morder = nullptr;      // [G] members by descending arc count (persistent CTAs take the heavy ones first)
     Sched fwd, bwd;
     Sched vit;        // forward (in-arc) schedule with natural-log weights for fb_viterbi
-    int vit_ok = 0;   // the Viterbi schedule fits shared memory
+    int vit_ok = 0;   // the Viterbi schedule was built (K ≤ 8192: 16-bit byte offsets into float64 u)
+    int vit_global = 0; // ... but does not fit shared memory: k_viterbi streams it from global memory (L2)
     PdfMap pm;
     CPlan cp;         // cluster plan (k_fbc); cp.ok == 0: one CTA per sequence (k_fb)
     LitPlan lit;      // the paper's literal block-diagonal strategy (fb_literal.cu, N4)
@@ -233,7 +234,7 @@ FBX_HD inline CLayout cl_layout(int rec_bytes, int K_int, int Kc_max, int Dc_max
 // Dynamic shared memory needed by a forward/backward launch over this graph.
 size_t smem_bytes(const Graph &g, bool backward, bool pdf_level);
 // ... and by a Viterbi launch (float64 u / best, int32 arg per state).
-size_t viterbi_smem_bytes(const Graph &g);
+size_t viterbi_smem_bytes(const Graph &g, bool global_sched = false);
 
 }  // namespace fbx
 

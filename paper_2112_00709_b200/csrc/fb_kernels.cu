@@ -122,6 +122,41 @@ __device__ __forceinline__ void phase_a_max(uint32_t cur, int nsl, int lane, uin
     }
 }
 
+// The same over a schedule left in global memory (graphs whose Viterbi schedule
+// exceeds shared memory, e.g. the paper's 50,984-arc denominator): records are
+// read through the read-only path (L2-resident: every CTA streams the same
+// blob each frame), four arc pairs in flight per lane.
+__device__ __forceinline__ void phase_a_max_g(const unsigned char *cur, int nsl, int lane, uint32_t a_u,
+                                              uint32_t a_best, uint32_t a_arg) {
+    for (int q = 0; q < nsl; ++q) {
+        const uint32_t h = __ldg((const uint32_t *)cur + lane);
+        const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
+        const uint32_t *ia = (const uint32_t *)(cur + 128) + lane;
+        const float2 *wa = (const float2 *)(cur + 128 + (size_t)L2 * 128) + lane;
+        double b0 = NEG_INF_D, b1 = NEG_INF_D;
+        int g0 = 0x7fffffff, g1 = 0x7fffffff;
+#pragma unroll 4
+        for (int s = 0; s < L2; ++s) {
+            const uint32_t ix = __ldg(ia + 32 * s);
+            const float2 w2 = __ldg(wa + 32 * s);
+            const uint32_t o0 = ix & 0xFFFFu, o1 = ix >> 16;
+            vit_consider(b0, g0, lds_v(a_u + o0, 0.0) + (double)w2.x, (int)(o0 >> 3));
+            vit_consider(b1, g1, lds_v(a_u + o1, 0.0) + (double)w2.y, (int)(o1 >> 3));
+        }
+        vit_consider(b0, g0, b1, g1);
+        for (int o = 1; o < (1 << lg); o <<= 1) {
+            const double bo = __shfl_xor_sync(0xffffffffu, b0, o);
+            const int go = __shfl_xor_sync(0xffffffffu, g0, o);
+            vit_consider(b0, g0, bo, go);
+        }
+        if (row >= 0) {
+            sts_v(a_best + (uint32_t)row * 8, b0);
+            sts_i(a_arg + (uint32_t)row * 4, b0 == NEG_INF_D ? -1 : g0);
+        }
+        cur += 128 + (size_t)L2 * 384;
+    }
+}
+
 struct VitArgs {
     Graph g;
     const float *emis;
@@ -138,7 +173,9 @@ struct VitArgs {
 // (Eq. (13) with ⊕ = max), backpointers to HBM, argmax of δ_{N-1} ⊗ ω,
 // backtrace by one thread.  Float64 values, no normalisation: scores are the
 // same float64 sums the oracle forms, so the tie-broken path agrees exactly.
-template <int SPT, int MAXT>
+// GLOB: the schedule stays in global memory (Graph::vit_global), shared memory
+// holds only the float64 vectors.
+template <int SPT, int MAXT, bool GLOB>
 __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const VitArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const Graph &G = a.g;
@@ -149,7 +186,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const 
     const int s0 = G.state_off[gi];
     const int K = G.state_off[gi + 1] - s0;
     const int N = a.lengths[b];
-    const SmemLayout SL = smem_layout(S.bytes_max, T * SPT, true, false);
+    const SmemLayout SL = smem_layout(GLOB ? 0 : S.bytes_max, T * SPT, true, false);
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t a_u = sb + (uint32_t)SL.u, a_best = sb + (uint32_t)SL.part;
     const uint32_t a_red = sb + (uint32_t)SL.red, a_arg = sb + (uint32_t)SL.total;
@@ -160,7 +197,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const 
         if (tid == 0) { a.score[b] = -INFINITY; a.status[b] = FB_SEQ_BAD_LENGTH; }
         return;
     }
-    {
+    if (!GLOB) {
         const uint4 *src = (const uint4 *)(S.rec + S.rec_off[gi]);
         uint4 *dst = (uint4 *)(smem_raw + SL.rec);
         const int n16 = S.rec_bytes[gi] >> 4;
@@ -168,6 +205,7 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const 
     }
     const int nsl = S.warp_nsl[gi * W + warp];
     const uint32_t mysl = sb + (uint32_t)SL.rec + (uint32_t)S.warp_off[gi * W + warp];
+    const unsigned char *mysl_g = S.rec + S.rec_off[gi] + S.warp_off[gi * W + warp];
     int pdfk[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
@@ -190,7 +228,8 @@ __global__ void __launch_bounds__(MAXT, (MAXT == 1024 ? 1 : 2)) k_viterbi(const 
     }
     for (int n = 1; n < N; ++n) {
         __syncthreads();
-        phase_a_max(mysl, nsl, lane, a_u, a_best, a_arg);
+        if (GLOB) phase_a_max_g(mysl_g, nsl, lane, a_u, a_best, a_arg);
+        else phase_a_max(mysl, nsl, lane, a_u, a_best, a_arg);
         __syncthreads();
         const float *row = em + (size_t)n * a.D;
 #pragma unroll
@@ -837,15 +876,19 @@ extern "C" fb_status fb_viterbi(fb_graph g, const float *log_emis, const int32_t
     using VFn = void (*)(VitArgs);
     VFn fn;
     const bool small = G.T <= 256;
+    const bool glob = G.vit_global != 0;
+#define FBX_VIT(S) (glob ? (small ? k_viterbi<S, 256, true> : k_viterbi<S, 1024, true>) \
+                         : (small ? k_viterbi<S, 256, false> : k_viterbi<S, 1024, false>))
     switch (G.spt) {
-        case 1: fn = small ? k_viterbi<1, 256> : k_viterbi<1, 1024>; break;
-        case 2: fn = small ? k_viterbi<2, 256> : k_viterbi<2, 1024>; break;
-        case 3: fn = small ? k_viterbi<3, 256> : k_viterbi<3, 1024>; break;
-        case 4: fn = small ? k_viterbi<4, 256> : k_viterbi<4, 1024>; break;
-        case 6: fn = small ? k_viterbi<6, 256> : k_viterbi<6, 1024>; break;
-        default: fn = small ? k_viterbi<8, 256> : k_viterbi<8, 1024>; break;
+        case 1: fn = FBX_VIT(1); break;
+        case 2: fn = FBX_VIT(2); break;
+        case 3: fn = FBX_VIT(3); break;
+        case 4: fn = FBX_VIT(4); break;
+        case 6: fn = FBX_VIT(6); break;
+        default: fn = FBX_VIT(8); break;
     }
-    const size_t sm = viterbi_smem_bytes(G);
+#undef FBX_VIT
+    const size_t sm = viterbi_smem_bytes(G, glob);
     if (fb_status r0 = set_smem((const void *)fn, sm); r0 != FB_OK) return r0;
     cudaStream_t s = (cudaStream_t)stream;
     {

@@ -296,6 +296,16 @@ def test_viterbi_c3_den(fbx):
     _viterbi_check(fbx, w.den, w.emis, np.array([80, 13, 1, 55], np.int32))
 
 
+def test_viterbi_paper_shape_n2(fbx):
+    """N1 on the paper's Table 1 denominator (3022 states, 50,984 arcs): its
+    float64 Viterbi schedule exceeds shared memory and is streamed from global memory
+    (L2); scores and tie-broken paths equal the oracle's bit for bit."""
+    w = synth.make_paper_shape(seed=6, B=3, N=60, L_range=(10, 20))
+    g = fbx.Graph.from_host(w.den)
+    assert g.info["cluster_C"] > 0  # the one-CTA forward-backward kernels do not fit either
+    _viterbi_check(fbx, w.den, w.emis, np.array([60, 41, 1], np.int32))
+
+
 # ------------------------------------------------------------------ cluster-batched kernel (k_fbc)
 
 @pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2", "4,4,1", "4,4,1/split0", "2,2/split1",
