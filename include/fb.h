@@ -279,6 +279,26 @@ fb_status fb_forward_literal(fb_graph g, int32_t semiring, const float *log_emis
                              void *stream);
 
 /*
+ * fb_forward_backward_literal — the literal strategy's full forward-backward
+ * (SURVEY §8(f) N4): fb_forward_literal's forward storing every frame's batch
+ * vector X_n, then the backward of the same block-diagonal matrix, one SpMV per
+ * frame over the augmented out-arc lists (Eq. (14) with v_{n+1}, ledger L2,
+ * P:179-181; y_{N_max} = 1̄ on each phony state), writing the frame's
+ * posteriors (Eq. (15), semifield division, ledger L5) in the same launch:
+ *   post[b,n,k] = X_n(k) ⊗ y_n(k) ⊘ score[b]   for n < N_b, real states k; else 0,
+ * with post in the lattice layout of fb_forward (may be NULL: score only), float64.
+ *   FB_SEMIRING_LOG       γ = exp(x + y − log Z)  (the state posteriors of fb_backward)
+ *   FB_SEMIRING_PROB      γ = x·y / Z             (linear domain; 0 where Z underflows)
+ *   FB_SEMIRING_TROPICAL  exp(x + y − best) ∈ [0, 1], the max-marginal ratio: 1 on
+ *                         the states of a best path (fb_viterbi's), < 1 elsewhere.
+ * workspace ≥ fb_literal_fb_workspace_bytes(g, B, N_max) ((N_max + 3) batch vectors).
+ */
+size_t fb_literal_fb_workspace_bytes(fb_graph g, int32_t B, int32_t N_max);
+fb_status fb_forward_backward_literal(fb_graph g, int32_t semiring, const float *log_emis, const int32_t *lengths,
+                                      int32_t B, int32_t N_max, double *score, double *post, void *workspace,
+                                      size_t workspace_bytes, void *stream);
+
+/*
  * Kernel timing (tracing).  When enabled, every kernel the library launches is
  * bracketed by cudaEventRecord on the stream it is launched on.
  * fb_profile_collect synchronises those events and returns, per kernel name,

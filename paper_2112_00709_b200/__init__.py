@@ -25,7 +25,7 @@ from ._lib import EXPORTS, lib  # noqa: F401
 
 __all__ = [
     "FBError", "Graph", "fb_forward", "fb_backward", "fb_posteriors", "fb_gap", "lfmmi_loss_grad", "workspace_bytes",
-    "fb_viterbi", "fb_forward_literal", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
+    "fb_viterbi", "fb_forward_literal", "fb_forward_backward_literal", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
     "SEMIRING_LOG", "SEMIRING_TROPICAL", "SEMIRING_PROB",
     "SEQ_OK", "SEQ_EMPTY_LATTICE", "SEQ_NONFINITE_INPUT", "SEQ_BAD_LENGTH",
     "GRAPH_DEFAULT", "GRAPH_FORCE_EXACT", "GRAPH_FORCE_FACTORED", "GRAPH_CLUSTER",
@@ -377,6 +377,26 @@ def fb_forward_literal(g: Graph, emis, lengths, semiring: int = SEMIRING_LOG):
                                     _dev(score, torch.float64, "score"), _dev(ws, torch.uint8, "workspace"),
                                     ws.numel(), _stream()), "fb_forward_literal")
     return score
+
+
+def fb_forward_backward_literal(g: Graph, emis, lengths, semiring: int = SEMIRING_LOG, want_post: bool = True):
+    """The literal strategy's forward-backward (N4): one batch SpMV per frame in each
+    direction, posteriors X ⊗ y ⊘ Z in the semiring.  Returns (score [B] f64, post f64
+    in the lattice layout, or None)."""
+    import torch
+
+    B, N_max, D = _check_inputs(g, emis, lengths, "fb_forward_backward_literal")
+    dev = emis.device
+    nbytes = int(lib().fb_literal_fb_workspace_bytes(g.handle, B, N_max))
+    ws = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    post = torch.empty(g.lattice_numel(B, N_max), dtype=torch.float64, device=dev) if want_post else None
+    _check(lib().fb_forward_backward_literal(g.handle, int(semiring), _dev(emis, torch.float32, "emis"),
+                                             _dev(lengths, torch.int32, "lengths"), B, N_max,
+                                             _dev(score, torch.float64, "score"), _dev(post, torch.float64, "post"),
+                                             _dev(ws, torch.uint8, "workspace"), ws.numel(), _stream()),
+           "fb_forward_backward_literal")
+    return score, post
 
 
 def profile_enable(on: bool = True) -> None:

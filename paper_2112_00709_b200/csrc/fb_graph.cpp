@@ -596,6 +596,8 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     RowLists in0, out0;  // member 0's arc lists (cluster plan of a shared graph)
     std::vector<int> lit_row_off(G), lit_ptr(1, 0), lit_src, lit_inst(G + 1, 0);
     std::vector<double> lit_w;
+    std::vector<int> lit_optr(1, 0), lit_odst;  // out-arc lists (same row numbering as lit_ptr)
+    std::vector<double> lit_ow;
     for (int g = 0; g < G; ++g) {
         const int s0 = state_offsets[g], K = state_offsets[g + 1] - s0;
         RowLists in, outl;
@@ -684,6 +686,22 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
         lit_w.push_back(0.0);
         lit_ptr.push_back((int)lit_src.size());
         lit_inst[g + 1] = lit_inst[g] + K + 1;
+        // out-arc lists of the same augmented block (backward pass, Eq. (14)): state
+        // s → its successors, then s → phony weighted ω(s); phony → phony (1̄)
+        for (int i = 0; i < K; ++i) {
+            for (int a2 = outl.ptr[i]; a2 < outl.ptr[i + 1]; ++a2) {
+                lit_odst.push_back(outl.other[a2]);
+                lit_ow.push_back(outl.w[a2]);
+            }
+            if (!(std::isinf(log_final[s0 + i]) && log_final[s0 + i] < 0)) {
+                lit_odst.push_back(K);
+                lit_ow.push_back(log_final[s0 + i]);
+            }
+            lit_optr.push_back((int)lit_odst.size());
+        }
+        lit_odst.push_back(K);
+        lit_ow.push_back(0.0);
+        lit_optr.push_back((int)lit_odst.size());
         if (G == 1) { in0 = std::move(in); out0 = std::move(outl); }
     }
     gr.fwd.bytes_max = hf.bytes_max; gr.fwd.slots_max = hf.slots_max;
@@ -750,7 +768,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     };
     SO of = put_sched(hf), ob = put_sched(hb), ov = put_sched(hv);
     size_t o_lro = pk.put(lit_row_off), o_lp = pk.put(lit_ptr), o_ls = pk.put(lit_src), o_lw = pk.put(lit_w),
-           o_li = pk.put(lit_inst);
+           o_li = pk.put(lit_inst), o_lop = pk.put(lit_optr), o_lod = pk.put(lit_odst), o_low = pk.put(lit_ow);
     SO ocf{}, ocb{};
     size_t o_cpo = 0, o_cpl = 0, o_cpe = 0, o_cpd = 0, o_cdf = 0, o_cds = 0, o_ci2 = 0, o_cf2 = 0, o_cpq = 0,
            o_fp = 0, o_fs = 0, o_fw = 0, o_bp = 0, o_bs = 0, o_bw = 0;
@@ -814,6 +832,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     set_sched(gr.vit, ov);
     gr.lit.row_off = (const int *)P(o_lro); gr.lit.ptr = (const int *)P(o_lp); gr.lit.src = (const int *)P(o_ls);
     gr.lit.w = (const double *)P(o_lw); gr.lit.inst_off = (const int *)P(o_li);
+    gr.lit.optr = (const int *)P(o_lop); gr.lit.odst = (const int *)P(o_lod); gr.lit.ow = (const double *)P(o_low);
     gr.lit.g1 = G == 1; gr.lit.K1 = gr.K_max + 1; gr.lit.inst_total = lit_inst[G];
     if (cp_ok) {
         CPlan &c = gr.cp;

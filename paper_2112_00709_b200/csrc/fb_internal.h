@@ -108,6 +108,9 @@ struct LitPlan {
     const int *src = nullptr;       // local source ids (K_g = the phony state)
     const double *w = nullptr;      // natural-log weights (ω for phony arcs, 0 for its self-loop)
     const int *inst_off = nullptr;  // G == B: [B + 1] = state_off[b] + b
+    const int *optr = nullptr;      // out-arc lists of the same rows (backward pass): [Σ_g (K_g + 1) + 1]
+    const int *odst = nullptr;      // local destination ids (K_g = the phony state)
+    const double *ow = nullptr;     // natural-log weights (ω for arcs into phony, 0 for its self-loop)
     int g1 = 1, K1 = 0;             // G == 1: every instance has K + 1 rows
     long long inst_total = 0;       // G == B: Σ_b (K_b + 1)
     FBX_HD2 long long rows_per_batch(int B) const { return g1 ? (long long)B * K1 : inst_total; }

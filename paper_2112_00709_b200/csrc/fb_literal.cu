@@ -102,6 +102,65 @@ __global__ void __launch_bounds__(256) k_literal_frame(const Graph G, const floa
     }
 }
 
+// Backward frame of the same batch matrix (Eq. (14) with ledger L2):
+//   y_n(i) = ⊕_{i→j} T'_ij ⊗ v_{n+1}(j) ⊗ y_{n+1}(j),   y_{N_max} = 1̄ on phony, 0̄ elsewhere
+// (the final weights live on the arcs into phony), over the augmented out-arc
+// lists; the same launch writes the frame's posteriors (Eq. (15), read as
+// semifield division, ledger L5) from the stored forward lattice X:
+//   post_n(k) = X_n(k) ⊗ y_n(k) ⊘ Z_b,   Z_b = X_{N_max}(phony_b)
+// for real states k and n < N_b (0 otherwise; layout of fb.h: [B][N_max][K] for
+// G == 1, packed per sequence for G == B).  Log: γ = exp(x + y − log Z); prob:
+// γ = x·y / Z; tropical: the max-marginal ratio exp(x + y − best) ∈ [0, 1], 1 on
+// the states a best path visits.
+template <int SR>
+__global__ void __launch_bounds__(256) k_literal_bwd_frame(const Graph G, const float *emis, const int *lengths,
+                                                           int B, int N_max, int n, const double *X,
+                                                           const double *y_next, double *y_cur, double *post) {
+    using R = Semiring<SR>;
+    const LitPlan &P = G.lit;
+    const long long rows = P.rows_per_batch(B);
+    for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += (long long)gridDim.x * blockDim.x) {
+        int b, j;
+        P.locate(r, B, b, j);
+        const int g = (G.G == 1) ? 0 : b;
+        const int s0 = G.state_off[g];
+        const int K = G.state_off[g + 1] - s0;
+        const int N = lengths[b];
+        const long long base = r - j;
+        double y;
+        if (n == N_max) {
+            y = (j == K) ? R::one() : R::zero();
+        } else {
+            typename R::Acc acc;
+            const int row = P.row_off[g] + j;
+            for (int e = P.optr[row]; e < P.optr[row + 1]; ++e) {
+                const int d = P.odst[e];
+                double v;  // v_{n+1}(d)
+                if (d == K) v = (n + 1 < N) ? R::zero() : R::one();
+                else if (n + 1 >= N) v = R::zero();
+                else {
+                    const double phi = (double)emis[((size_t)b * N_max + n + 1) * G.D + G.pdf[s0 + d]];
+                    v = (SR == FB_SEMIRING_PROB) ? exp(phi) : phi;
+                }
+                acc.add(R::times(R::times(R::lift_w(P.ow[e]), v), y_next[base + d]));
+            }
+            y = acc.value();
+        }
+        y_cur[r] = y;
+        if (post && j < K && n < N_max) {
+            const size_t o = (G.G == 1 ? (size_t)b * N_max * K : (size_t)N_max * s0) + (size_t)n * K + j;
+            const double Z = X[(size_t)N_max * rows + base + K];  // x_{N_max}(phony_b)
+            double gam = 0.0;
+            if (n < N && N <= N_max) {
+                const double xy = R::times(X[(size_t)n * rows + r], y);
+                if (SR == FB_SEMIRING_PROB) gam = (Z > 0.0) ? xy / Z : 0.0;
+                else gam = (Z > -INFINITY && xy > -INFINITY) ? exp(xy - Z) : 0.0;
+            }
+            post[o] = gam;
+        }
+    }
+}
+
 // Host driver: N_max + 1 launches (one SpMV per frame), ping-pong state vectors in the workspace.
 template <int SR>
 static fb_status run_literal(const Graph &G, const float *emis, const int *lengths, int B, int N_max, double *score,
@@ -118,9 +177,55 @@ static fb_status run_literal(const Graph &G, const float *emis, const int *lengt
     return FB_OK;
 }
 
+// Forward storing every frame's batch vector X_n (n = 0 … N_max), then N_max + 1
+// backward launches writing the posteriors frame by frame.
+template <int SR>
+static fb_status run_literal_fb(const Graph &G, const float *emis, const int *lengths, int B, int N_max, double *score,
+                                double *post, double *X, double *y0, double *y1, cudaStream_t s) {
+    const long long rows = G.lit.rows_per_batch(B);
+    const int grid = (int)std::min<long long>((rows + 255) / 256, 148 * 16);
+    for (int n = 0; n <= N_max; ++n)
+        k_literal_frame<SR><<<grid, 256, 0, s>>>(G, emis, lengths, B, N_max, n, X + (size_t)(n ? n - 1 : 0) * rows,
+                                                 X + (size_t)n * rows, score);
+    for (int n = N_max; n >= 0; --n) {
+        const double *yn = (n & 1) ? y0 : y1;
+        double *yc = (n & 1) ? y1 : y0;
+        k_literal_bwd_frame<SR><<<grid, 256, 0, s>>>(G, emis, lengths, B, N_max, n, X, yn, yc, post);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_cuda_error("k_literal launch", (int)e); return FB_ERR_CUDA; }
+    return FB_OK;
+}
+
 }  // namespace fbx
 
 using namespace fbx;
+
+extern "C" size_t fb_literal_fb_workspace_bytes(fb_graph g, int32_t B, int32_t N_max) {
+    if (!g || B < 1 || N_max < 1 || !(g->g.G == 1 || g->g.G == B)) return 0;
+    return ((size_t)N_max + 3) * (size_t)g->g.lit.rows_per_batch(B) * sizeof(double) + 256;
+}
+
+extern "C" fb_status fb_forward_backward_literal(fb_graph g, int32_t semiring, const float *log_emis,
+                                                 const int32_t *lengths, int32_t B, int32_t N_max, double *score,
+                                                 double *post, void *workspace, size_t workspace_bytes, void *stream) {
+    if (!g || !log_emis || !lengths || !score || B < 1 || N_max < 1) return FB_ERR_INVALID_ARG;
+    if (!(g->g.G == 1 || g->g.G == B) || g->g.dry) return FB_ERR_INVALID_ARG;
+    if (!workspace || workspace_bytes < fb_literal_fb_workspace_bytes(g, B, N_max)) return FB_ERR_WORKSPACE;
+    const Graph &G = g->g;
+    const size_t rows = (size_t)G.lit.rows_per_batch(B);
+    double *X = (double *)workspace, *y0 = X + ((size_t)N_max + 1) * rows, *y1 = y0 + rows;
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (semiring) {
+        case FB_SEMIRING_LOG:
+            return run_literal_fb<FB_SEMIRING_LOG>(G, log_emis, lengths, B, N_max, score, post, X, y0, y1, s);
+        case FB_SEMIRING_TROPICAL:
+            return run_literal_fb<FB_SEMIRING_TROPICAL>(G, log_emis, lengths, B, N_max, score, post, X, y0, y1, s);
+        case FB_SEMIRING_PROB:
+            return run_literal_fb<FB_SEMIRING_PROB>(G, log_emis, lengths, B, N_max, score, post, X, y0, y1, s);
+        default: return FB_ERR_INVALID_ARG;
+    }
+}
 
 extern "C" size_t fb_literal_workspace_bytes(fb_graph g, int32_t B) {
     if (!g || B < 1 || !(g->g.G == 1 || g->g.G == B)) return 0;

@@ -108,3 +108,78 @@ def test_prob_semiring_equals_exp_logZ_and_underflows(fbx):
     lz = literal(fbx, lr, e, L, fbx.SEMIRING_LOG)[0]
     ref = oracle.fb_batch(lr, e, L, post=False)["logZ"][0]
     assert np.isfinite(lz) and abs(lz - ref) <= 1e-12 * abs(ref)
+
+
+# ------------------------------------------------------------------ forward-backward + posteriors (N4)
+
+def literal_fb(fbx, graph, emis, lengths, sr):
+    import torch
+
+    g = fbx.Graph.from_host(graph)
+    score, post = fbx.fb_forward_backward_literal(g, dev(emis.astype(np.float32)), dev(lengths.astype(np.int32)), sr)
+    torch.cuda.synchronize()
+    return score.cpu().numpy(), post.cpu().numpy()
+
+
+@pytest.mark.parametrize("which", ["c1", "small", "c2", "den"])
+def test_literal_fb_log_posteriors_vs_oracle(fbx, which):
+    """Log semiring: the literal backward over the augmented out-arc lists and the
+    posteriors X ⊗ y ⊘ Z equal the oracle's γ (float64 both sides) on the C1 batch,
+    the irregular brute-force family (−∞ / duplicate arcs, weighted π/ω, ragged
+    lengths), numerator graphs (G = B) and a shared den (G = 1)."""
+    if which == "c1":
+        ws = [synth.make_c1(s) for s in range(30)]
+        g = synth.compose([w.den for w in ws])
+        emis = np.concatenate([w.emis for w in ws])
+        lens = np.full(30, 6, np.int32)
+        lens[::4] = 2
+    elif which == "small":
+        rng = np.random.Generator(np.random.PCG64(77))
+        gs = [synth.random_small_graph(rng, K=int(rng.integers(1, 7)), D=6) for _ in range(60)]
+        g = synth.compose(gs)
+        emis = rng.uniform(-3, 0, (60, 7, 6)).astype(np.float32)
+        lens = rng.integers(1, 8, 60).astype(np.int32)
+    elif which == "c2":
+        w = synth.make_c2(seed=4, B=6)
+        g, emis, lens = synth.compose(w.nums), w.emis, w.lengths
+    else:
+        w = synth.make_c3(seed=35, B=3, N=30, K=700, nnz=4000)
+        g, emis, lens = w.den, w.emis, np.array([30, 11, 30], np.int32)
+    score, post = literal_fb(fbx, g, emis, lens, fbx.SEMIRING_LOG)
+    ref = oracle.fb_batch(g, emis, lens, post=True)
+    ok = ref["status"] == 0
+    assert np.abs(score[ok] - ref["logZ"][ok]).max(initial=0) <= 1e-11 * max(1.0, np.abs(ref["logZ"][ok]).max())
+    assert np.isneginf(score[~ok]).all()
+    assert np.abs(post.reshape(ref["post"].shape) - ref["post"]).max() <= 1e-11
+
+
+def test_literal_fb_prob_and_tropical(fbx):
+    """Probability semiring: the same γ in the linear domain (short inputs).  Tropical:
+    the max-marginal ratio is 1 exactly along fb_viterbi's best path (unique here) and
+    ≤ 1 everywhere."""
+    import torch
+
+    w = synth.make_c2(seed=5, B=4, N_max=150)
+    g, emis = synth.compose(w.nums), w.emis
+    lens = np.minimum(w.lengths, 150)
+    ref = oracle.fb_batch(g, emis, lens, post=True)
+    ws = [synth.make_c1(s) for s in range(10)]
+    g1 = synth.compose([x.den for x in ws])
+    e1 = np.concatenate([x.emis for x in ws])
+    l1 = np.full(10, 6, np.int32)
+    sp, pp = literal_fb(fbx, g1, e1, l1, fbx.SEMIRING_PROB)
+    r1 = oracle.fb_batch(g1, e1, l1, post=True)
+    assert (np.abs(sp - np.exp(r1["logZ"])) / np.exp(r1["logZ"])).max() <= 1e-12
+    assert np.abs(pp.reshape(r1["post"].shape) - r1["post"]).max() <= 1e-11
+    st, pt = literal_fb(fbx, g, emis, lens, fbx.SEMIRING_TROPICAL)
+    vit = oracle.viterbi_batch(g, emis, lens)
+    assert np.abs(st - vit["score"]).max() <= 1e-9 * np.abs(vit["score"]).max()
+    so = g.state_offsets
+    N_max = emis.shape[1]
+    for b in range(len(lens)):
+        K = so[b + 1] - so[b]
+        P = pt[N_max * so[b]: N_max * so[b + 1]].reshape(N_max, K)
+        assert (P <= 1 + 1e-9).all() and (P[lens[b]:] == 0).all()
+        path = vit["path"][b, : lens[b]]
+        assert np.abs(P[np.arange(lens[b]), path] - 1).max() <= 1e-9
+    torch.cuda.synchronize()
