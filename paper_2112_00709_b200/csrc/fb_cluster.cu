@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             for (int j = tid; j < Kc; j += T) {
                 const int o = P.perm[k0 + j];
                 if (o < 0) continue;
-                if (lattice && a.lat) a.lat[rowb * K + o] = NEG_INF;
+                if (lattice && a.lat && !a.lat_int) a.lat[rowb * K + o] = NEG_INF;
                 if (want_post && a.post_kind == POST_STATE) a.post[rowb * K + o] = 0.f;
             }
             if (pdf_post)
@@ -349,6 +349,12 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const bool act = t < Ns[s];
+            if (a.lat_int) {  // internal order: this CTA's part rows are contiguous
+                const float *ro = a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * Kint : 0) + k0 + tid;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + k * T) : NEG_INF;
+                continue;
+            }
             const float *ro = a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * K : 0);
 #pragma unroll
             for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + origk[k]) : NEG_INF;
@@ -427,6 +433,13 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (t >= Ns[s]) continue;
+            if (a.lat_int) {
+                float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * Kint + k0 + tid;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k)
+                    if (tid + k * T < Kc) latn[k * T] = h[k][s] * LN2;
+                continue;
+            }
             float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * K;
 #pragma unroll
             for (int k = 0; k < SPT; ++k)

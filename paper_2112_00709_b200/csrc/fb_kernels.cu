@@ -681,7 +681,8 @@ static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 static WsLayout ws_layout(const Graph &num, const Graph &den, int B, int N_max) {
     WsLayout w;
     size_t o = 0;
-    w.den_alpha = o; o += a256((size_t)B * N_max * den.K_tot * 4);
+    // den α̂: rows of K (one CTA per sequence) or of the cluster plan's K_int (internal order)
+    w.den_alpha = o; o += a256((size_t)B * N_max * std::max(den.K_tot, den.cp.ok ? den.cp.K_int : 0) * 4);
     w.num_alpha = o; o += a256((size_t)N_max * num.K_tot * 8);  // float64 when the numerator runs raw
     w.gnum = o; o += a256((size_t)N_max * num.pm.U_tot * 4);
     w.zn = o; o += a256((size_t)B * 8);
@@ -800,7 +801,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     cudaEventRecord(sr->fork, s);
     {
         FBArgs a = base_args(den, log_emis, lengths, B, N_max);
-        a.lat = den_alpha; a.logZ = zd; a.status = seq_status;
+        a.lat = den_alpha; a.logZ = zd; a.status = seq_status; a.lat_int = 1;
         if ((r = launch_fb(false, a, s)) != FB_OK) return r;
     }
     cudaStreamWaitEvent(sr->s, sr->fork, 0);
@@ -826,7 +827,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     // denominator backward + fused −Γ_den gradient epilogue: independent of the numerator
     {
         FBArgs c = base_args(den, log_emis, lengths, B, N_max);
-        c.status = seq_status; c.alpha = den_alpha;
+        c.status = seq_status; c.alpha = den_alpha; c.lat_int = 1;
         c.post = grad; c.post_kind = POST_GRAD;
         if ((r = launch_fb(true, c, s)) != FB_OK) return r;
     }
