@@ -567,6 +567,9 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
     // many small exact-mode members (a batch of numerator graphs): ≤ 256 threads per CTA
     // while ≤ 4 states per thread suffice, so more utterances run concurrently per SM
     if (gr.mode == MODE_EXACT && G > 1 && T > 256 && (gr.K_max + 255) / 256 <= 4) T = 256;
+    // ... and 128 while ≤ 4 states per thread suffice (N2's 454-state numerators: 7 CTAs
+    // per SM instead of 2, so every utterance of a 128-batch is resident on the idle SMs)
+    if (gr.mode == MODE_EXACT && G > 1 && T > 128 && (gr.K_max + 127) / 128 <= 4) T = 128;
     if (const char *e = std::getenv("FBX_EXACT_T"); e && gr.mode == MODE_EXACT) T = std::max(128, std::atoi(e));
     if (const char *e = std::getenv("FBX_FACT_T"); e && gr.mode == MODE_FACTORED) T = std::max(128, std::atoi(e));
     T = std::max(T, std::min(1024, pow2ceil((gr.K_max + kMaxSPT - 1) / kMaxSPT)));
