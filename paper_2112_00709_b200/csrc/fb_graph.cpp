@@ -51,6 +51,11 @@ struct RowLists {
     std::vector<double> w;  // natural log
 };
 
+// Tie-break keys for slice formation while compiling a relabelled graph (the
+// original state id of each new id), so that its slices hold the same rows as the
+// original compile's; null otherwise.  Set only around the nested create.
+thread_local const std::vector<int> *g_tie = nullptr;
+
 // Grouped sliced-ELL schedule for one member graph (appends to hs); see Sched.
 // esize = bytes per element of the gathered u / p arrays; index words hold byte
 // offsets relative to the gathered array and are rebased to shared-memory
@@ -73,7 +78,12 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     std::vector<Slice> sl;
     for (int lg = 0; lg < 6; ++lg) {
         auto &c = cls[lg];
-        std::stable_sort(c.begin(), c.end(), [](const RowG &a, const RowG &b) { return a.len > b.len; });
+        if (g_tie)  // relabelled compile: ties in the original state order (same slices as the original)
+            std::stable_sort(c.begin(), c.end(), [](const RowG &a, const RowG &b) {
+                return a.len != b.len ? a.len > b.len : (*g_tie)[a.row] < (*g_tie)[b.row];
+            });
+        else
+            std::stable_sort(c.begin(), c.end(), [](const RowG &a, const RowG &b) { return a.len > b.len; });
         const int per = 32 >> lg;
         for (size_t i = 0; i < c.size(); i += per) {
             Slice s;
@@ -490,11 +500,233 @@ size_t smem_bytes(const Graph &g, bool backward, bool post) {
     return smem_layout(s.bytes_max, g.T * g.spt, g.mode == MODE_EXACT, backward && post).total;
 }
 
+// ---------------------------------------------------------------- bank-aware relabelling
+//
+// Shared-memory cost model of one frame of the one-CTA kernels (32 banks of 4
+// bytes; a state's bank is its id mod 32):
+//   • gathers: a slice with L slots per lane is conflict-free after the per-slice
+//     edge colouring iff no bank holds more than L of its arcs (König), else it
+//     costs about max_b(arcs in bank b) wavefronts: cost_g = max(L, max_b h[b]);
+//   • part-row stores: the slice's row leaders write part[row]: max_b (rows in b);
+//   • emission gathers of phase B: thread t owns ids t + kT, so each aligned block
+//     of 32 ids gathers φ[pdf] from the staged row: max_b (states with pdf ≡ b).
+// Both directions' slices (in-arcs / out-arcs) and the emission blocks (read in
+// both) are summed.  A seeded local search over swaps of two ids accepts moves
+// that do not raise the total; the slice membership (rows grouped by length, ties
+// in original order) does not depend on the labelling.
+struct RelabelDir {
+    std::vector<int> L;                              // slots per lane of slice s
+    std::vector<std::vector<std::pair<int, int>>> src;  // state → (slice, #arcs gathered from it)
+    std::vector<int> lead;                           // state → slice it is a row of (−1 none)
+};
+
+static RelabelDir relabel_slices(const RowLists &rl, int K, int Lmax) {
+    RelabelDir R;
+    R.lead.assign(K, -1);
+    R.src.assign(K, {});
+    struct RowG { int row, len; };
+    std::vector<RowG> cls[6];
+    for (int r = 0; r < K; ++r) {
+        long long d = rl.ptr[r + 1] - rl.ptr[r];
+        if (d == 0) continue;
+        int lg = 0;
+        while (lg < 5 && (d + (1LL << lg) - 1) / (1LL << lg) > Lmax) ++lg;
+        cls[lg].push_back({r, (int)((d + (1LL << lg) - 1) / (1LL << lg))});
+    }
+    for (int lg = 0; lg < 6; ++lg) {
+        auto &c = cls[lg];
+        std::stable_sort(c.begin(), c.end(), [](const RowG &a, const RowG &b) { return a.len > b.len; });
+        const int per = 32 >> lg;
+        for (size_t i = 0; i < c.size(); i += per) {
+            const int sid = (int)R.L.size();
+            R.L.push_back((c[i].len + 1) & ~1);
+            std::vector<int> cnt;
+            for (size_t t = i; t < std::min(c.size(), i + per); ++t) {
+                const int r = c[t].row;
+                R.lead[r] = sid;
+                for (int a = rl.ptr[r]; a < rl.ptr[r + 1]; ++a) {
+                    auto &v = R.src[rl.other[a]];
+                    if (!v.empty() && v.back().first == sid) v.back().second++;
+                    else v.push_back({sid, 1});
+                }
+            }
+        }
+    }
+    return R;
+}
+
+// Returns pos[state] = new id (a permutation of 0 … K−1).
+static std::vector<int> bank_relabel(const RowLists &in, const RowLists &outl, int K, int Lmax,
+                                     const std::vector<int> &pdf, long long iters, bool verbose) {
+    RelabelDir dir[2] = {relabel_slices(in, K, Lmax), relabel_slices(outl, K, Lmax)};
+    const int NB = 32;
+    std::vector<int> pos(K), at(K);
+    std::iota(pos.begin(), pos.end(), 0);
+    std::iota(at.begin(), at.end(), 0);
+    // histograms
+    std::vector<std::vector<int>> hg[2], hl[2];
+    std::vector<int> cg[2], cl[2];
+    for (int d = 0; d < 2; ++d) {
+        const int ns = (int)dir[d].L.size();
+        hg[d].assign(ns, std::vector<int>(NB, 0));
+        hl[d].assign(ns, std::vector<int>(NB, 0));
+        for (int x = 0; x < K; ++x) {
+            for (auto &sc : dir[d].src[x]) hg[d][sc.first][pos[x] % NB] += sc.second;
+            if (dir[d].lead[x] >= 0) hl[d][dir[d].lead[x]][pos[x] % NB]++;
+        }
+        cg[d].resize(ns);
+        cl[d].resize(ns);
+    }
+    const int ng = (K + NB - 1) / NB;
+    std::vector<std::vector<int>> he(ng, std::vector<int>(NB, 0));
+    std::vector<int> ce(ng);
+    for (int x = 0; x < K; ++x) he[pos[x] / NB][pdf[x] % NB]++;
+    auto mx = [&](const std::vector<int> &h) { int m = 0; for (int v : h) m = std::max(m, v); return m; };
+    long long total = 0;
+    for (int d = 0; d < 2; ++d)
+        for (size_t sl = 0; sl < dir[d].L.size(); ++sl) {
+            cg[d][sl] = std::max(dir[d].L[sl], mx(hg[d][sl]));
+            cl[d][sl] = mx(hl[d][sl]);
+            total += cg[d][sl] + cl[d][sl];
+        }
+    for (int g = 0; g < ng; ++g) { ce[g] = mx(he[g]); total += 2 * ce[g]; }
+    const long long start = total;
+    uint64_t rng = 0x2545F4914F6CDD1Dull ^ (uint64_t)K;
+    auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
+    std::vector<int> touched_s[2], touched_g;
+    auto apply = [&](int x, int from, int to) {  // move state x from id `from` to id `to` (histograms only)
+        for (int d = 0; d < 2; ++d) {
+            for (auto &sc : dir[d].src[x]) {
+                hg[d][sc.first][from % NB] -= sc.second;
+                hg[d][sc.first][to % NB] += sc.second;
+                touched_s[d].push_back(sc.first);
+            }
+            const int sl = dir[d].lead[x];
+            if (sl >= 0) { hl[d][sl][from % NB]--; hl[d][sl][to % NB]++; touched_s[d].push_back(sl); }
+        }
+        he[from / NB][pdf[x] % NB]--;
+        he[to / NB][pdf[x] % NB]++;
+        touched_g.push_back(from / NB);
+        touched_g.push_back(to / NB);
+    };
+    for (long long it = 0; it < iters; ++it) {
+        const int p1 = (int)(next() % (uint64_t)K), p2 = (int)(next() % (uint64_t)K);
+        if (p1 == p2 || (p1 % NB == p2 % NB && p1 / NB == p2 / NB)) continue;
+        const int x = at[p1], y = at[p2];
+        for (int d = 0; d < 2; ++d) touched_s[d].clear();
+        touched_g.clear();
+        apply(x, p1, p2);
+        apply(y, p2, p1);
+        long long delta = 0;
+        std::vector<std::pair<int, int>> newc[2];
+        for (int d = 0; d < 2; ++d) {
+            auto &ts = touched_s[d];
+            std::sort(ts.begin(), ts.end());
+            ts.erase(std::unique(ts.begin(), ts.end()), ts.end());
+            for (int sl : ts) {
+                const int g2 = std::max(dir[d].L[sl], mx(hg[d][sl])), l2 = mx(hl[d][sl]);
+                delta += (g2 - cg[d][sl]) + (l2 - cl[d][sl]);
+                newc[d].push_back({g2, l2});
+            }
+        }
+        std::sort(touched_g.begin(), touched_g.end());
+        touched_g.erase(std::unique(touched_g.begin(), touched_g.end()), touched_g.end());
+        std::vector<int> newe;
+        for (int g : touched_g) { const int e2 = mx(he[g]); delta += 2 * (e2 - ce[g]); newe.push_back(e2); }
+        if (delta <= 0) {
+            for (int d = 0; d < 2; ++d)
+                for (size_t i = 0; i < touched_s[d].size(); ++i) {
+                    cg[d][touched_s[d][i]] = newc[d][i].first;
+                    cl[d][touched_s[d][i]] = newc[d][i].second;
+                }
+            for (size_t i = 0; i < touched_g.size(); ++i) ce[touched_g[i]] = newe[i];
+            total += delta;
+            pos[x] = p2; pos[y] = p1; at[p1] = y; at[p2] = x;
+        } else {
+            for (int d = 0; d < 2; ++d) touched_s[d].clear();
+            touched_g.clear();
+            apply(x, p2, p1);
+            apply(y, p1, p2);
+        }
+    }
+    if (verbose) {
+        long long lsum = 0;
+        for (int d = 0; d < 2; ++d) for (int L : dir[d].L) lsum += L;
+        std::fprintf(stderr, "[fbx] bank relabel K=%d: modelled smem wavefronts/frame %lld -> %lld (floor %lld)\n", K,
+                     start, total, lsum + (long long)(dir[0].L.size() + dir[1].L.size()) + 2LL * ng);
+    }
+    return pos;
+}
+
 }  // namespace fbx
 
 using namespace fbx;
 
+static fb_status create_impl(fb_graph *out, int32_t G, const int32_t *state_offsets, const int32_t *row_ptr,
+                             const int32_t *col, const float *log_w, const float *log_init, const float *log_final,
+                             const int32_t *pdf_of, int32_t D, int32_t flags);
+
 extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *state_offsets,
+                                     const int32_t *row_ptr, const int32_t *col, const float *log_w,
+                                     const float *log_init, const float *log_final,
+                                     const int32_t *pdf_of, int32_t D, int32_t flags) {
+    fb_status r = create_impl(out, G, state_offsets, row_ptr, col, log_w, log_init, log_final, pdf_of, D, flags);
+    if (r != FB_OK) return r;
+    fb_graph h = *out;
+    const Graph &g = h->g;
+    // relabelled twin for the lfmmi denominator passes (one CTA per sequence, factored)
+    const bool stats_only = (flags & FB_GRAPH_DRY_RUN) && std::getenv("FBX_RELABEL_STATS");
+    if (G != 1 || g.mode != MODE_FACTORED || !g.legacy_ok || g.cp.ok || ((flags & FB_GRAPH_DRY_RUN) && !stats_only) ||
+        std::getenv("FBX_NO_RELABEL"))
+        return FB_OK;
+    const int K = g.K_tot;
+    RowLists in, outl;
+    in.ptr.assign(K + 1, 0);
+    outl.ptr.assign(K + 1, 0);
+    for (int i = 0; i < K; ++i) {
+        for (int a = row_ptr[i]; a < row_ptr[i + 1]; ++a) { outl.other.push_back(col[a]); in.ptr[col[a] + 1]++; }
+        outl.ptr[i + 1] = (int)outl.other.size();
+    }
+    for (int j = 0; j < K; ++j) in.ptr[j + 1] += in.ptr[j];
+    in.other.resize(outl.other.size());
+    {
+        std::vector<int> fill(K, 0);
+        for (int i = 0; i < K; ++i)
+            for (int a = outl.ptr[i]; a < outl.ptr[i + 1]; ++a) in.other[in.ptr[outl.other[a]] + fill[outl.other[a]]++] = i;
+    }
+    std::vector<int> pdf(K);
+    for (int i = 0; i < K; ++i) pdf[i] = pdf_of ? pdf_of[i] : i;
+    int lmax = 24;
+    if (const char *e = std::getenv("FBX_LMAX")) lmax = std::max(1, std::atoi(e));
+    long long iters = 100LL * K;
+    if (const char *e = std::getenv("FBX_RELABEL_ITERS")) iters = std::atoll(e);
+    const std::vector<int> pos = bank_relabel(in, outl, K, lmax, pdf, iters, std::getenv("FBX_RELABEL_STATS") != nullptr);
+    if (stats_only) return FB_OK;
+    std::vector<int> inv(K);
+    for (int i = 0; i < K; ++i) inv[pos[i]] = i;
+    // the permuted graph: new id q is original state inv[q]
+    std::vector<int32_t> rp(K + 1, 0), cl;
+    std::vector<float> lw, li(K), lf(K);
+    std::vector<int32_t> pd(K);
+    cl.reserve(col ? row_ptr[K] : 0);
+    for (int q = 0; q < K; ++q) {
+        const int i = inv[q];
+        for (int a = row_ptr[i]; a < row_ptr[i + 1]; ++a) { cl.push_back(pos[col[a]]); lw.push_back(log_w[a]); }
+        rp[q + 1] = (int32_t)cl.size();
+        li[q] = log_init[i];
+        lf[q] = log_final[i];
+        pd[q] = pdf[i];
+    }
+    fb_graph hp = nullptr;
+    g_tie = &inv;
+    r = create_impl(&hp, 1, state_offsets, rp.data(), cl.data(), lw.data(), li.data(), lf.data(), pd.data(), D,
+                    flags | FB_GRAPH_FORCE_FACTORED);
+    g_tie = nullptr;
+    if (r == FB_OK) h->perm = hp;  // any failure: lfmmi simply runs on the original labelling
+    return FB_OK;
+}
+
+static fb_status create_impl(fb_graph *out, int32_t G, const int32_t *state_offsets,
                                      const int32_t *row_ptr, const int32_t *col, const float *log_w,
                                      const float *log_init, const float *log_final,
                                      const int32_t *pdf_of, int32_t D, int32_t flags) {
@@ -861,6 +1093,7 @@ extern "C" fb_status fb_graph_create(fb_graph *out, int32_t G, const int32_t *st
 
 extern "C" fb_status fb_graph_destroy(fb_graph g) {
     if (!g) return FB_OK;
+    if (g->perm) fb_graph_destroy(g->perm);
     if (!g->g.dry) {
         cudaDeviceSynchronize();
         cudaFree(g->g.block);

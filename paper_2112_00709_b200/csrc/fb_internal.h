@@ -243,6 +243,12 @@ size_t viterbi_smem_bytes(const Graph &g, bool global_sched = false);
 
 struct fb_graph_s {
     fbx::Graph g;
+    // Shared factored graphs: the same graph with its states relabelled so that the
+    // shared-memory gathers, part-row stores and emission gathers of the one-CTA
+    // kernels hit distinct banks (fb_graph.cpp, bank_relabel).  lfmmi_loss_grad runs
+    // its denominator passes on it (their α̂ lattice is private and the gradient is
+    // pdf-level, so the labelling is invisible); the public lattice calls use g.
+    fb_graph_s *perm = nullptr;
     // dry-run handles keep the host image of the compiled schedules for inspection
     std::vector<unsigned char> host_fwd, host_bwd;
     std::vector<int> host_fwd_meta, host_bwd_meta;  // per member: rec_off, rec_bytes; then W × (warp_off, warp_nsl)

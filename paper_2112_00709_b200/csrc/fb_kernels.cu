@@ -777,6 +777,9 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
         return FB_ERR_INVALID_ARG;
     if (num->g.G != B || den->g.G != 1 || num->g.D != den->g.D || num->g.dry || den->g.dry)
         return FB_ERR_INVALID_ARG;
+    // the bank-relabelled twin of a shared factored graph (fb_graph.cpp): same sequences, same
+    // pdf-level gradient; only the private α̂ lattice is in its state order
+    if (den->perm) den = den->perm;
     WsLayout L = ws_layout(num->g, den->g, B, N_max);
     if (!workspace || workspace_bytes < L.total) return FB_ERR_WORKSPACE;
     unsigned char *ws = (unsigned char *)workspace;
