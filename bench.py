@@ -394,8 +394,8 @@ def run_ours(args, rank, world, local):
     for kname in ("k_fb", "k_fbc"):
         if c3:  # backward: φ row + α̂ row in, γ row out; forward: φ row in, α̂ row out
             alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Kw)
-        else:   # backward: φ row + α̂ row in, grad row out
-            alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Dw)
+        else:   # backward: φ row + α̂ row in, grad row out; padded frames' grad rows are written 0 (fb.h)
+            alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Dw) + (Bw * Nw - seq_frames) * 4 * Dw
         alg_bytes[kname + "_fwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw)
     kern = {}
     for name, (cnt, tot_ms) in prof.items():

@@ -172,13 +172,17 @@ __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uin
 
 // Exact max-then-sum of one row for sequence s over the previous frame's u
 // (fallback of the factored sum; accurate libm ops; rare).
-template <int S>
+// PV: the buffer holds p = 2^u (no-p plans): u = log2 p, and p = 0 (u below the fp32
+// range, 2^-126 under the frame's lagged maximum, or 0̄) reads as 0̄.
+template <int S, bool PV>
 static __device__ __noinline__ float exact_row_c(const int *ptr, const int *src, const float *w2, int row, int s,
                                                  uint32_t a_uprev, unsigned long long *ctr) {
     atomicAdd(ctr, 1ull);  // diagnostic: sequence-rows that needed the fallback (fb_graph_counters)
     float m = NEG_INF, sum = 0.f;
     for (int e = ptr[row]; e < ptr[row + 1]; ++e) {
-        const float x = lds_v(a_uprev + (uint32_t)(src[e] * S + s) * 4, 0.f) + w2[e];
+        float uv = lds_v(a_uprev + (uint32_t)(src[e] * S + s) * 4, 0.f);
+        if (PV) uv = uv > 0.f ? log2f(uv) : NEG_INF;
+        const float x = uv + w2[e];
         if (x == NEG_INF) continue;
         if (x > m) { sum = sum * exp2f(m - x) + 1.f; m = x; }
         else sum += exp2f(x - m);
@@ -382,7 +386,9 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 float pv[S];
 #pragma unroll
                 for (int s = 0; s < S; ++s) pv[s] = ex2(u[k][s]);
-                VS<S>::st(ub + (uint32_t)((k0 + j) * S) * 4, u[k]);
+                // no-p plans exchange and gather p = 2^u itself (one ex2 per owned element
+                // instead of one per gathered arc); with-p plans keep u and convert on receipt
+                VS<S>::st(ub + (uint32_t)((k0 + j) * S) * 4, NOP ? pv : u[k]);
                 if (!NOP) VS<S>::st(a_p + (uint32_t)((k0 + j) * S) * 4, pv);
             }
         }
@@ -583,7 +589,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             if (want_post) load_alpha(t);
             emis_issue(t + 1);
             // split: this part's own-source arcs while the other parts' rows are in flight
-            if (split) phase_a_vec<S, NOP>(mysl_loc, nsl_loc, lane, NOP ? a_u(t - 1) : a_p, a_part, true);
+            if (split) phase_a_vec<S, false>(mysl_loc, nsl_loc, lane, NOP ? a_u(t - 1) : a_p, a_part, true);
         }
         mbar_wait_sleep(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
         const uint32_t up = a_u(t - 1);
@@ -652,7 +658,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 }
             }
         }
-        if (!last) phase_a_vec<S, NOP>(mysl, nsl, lane, NOP ? up : a_p, a_part, split);
+        if (!last) phase_a_vec<S, false>(mysl, nsl, lane, NOP ? up : a_p, a_part, split);
         cpa_wait1();
         __syncthreads();  // part rows, γ rows, step-t emissions complete
         // pdf-level rows of frame t−1 for this part's pdf range (ascending states, ledger L9)
@@ -728,7 +734,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     if (!(distk[k] <= lim[s]) || (acc[s] >= kTiny && acc[s] <= kHuge)) continue;
-                    const float y = exact_row_c<S>(BWD ? P.bptr : P.fptr, BWD ? P.bsrc : P.fsrc, BWD ? P.bw2 : P.fw2,
+                    const float y = exact_row_c<S, NOP>(BWD ? P.bptr : P.fptr, BWD ? P.bsrc : P.fsrc, BWD ? P.bw2 : P.fw2,
                                                    k0 + j, s, up, G.ctr + 1);
                     const float v = lds_v(eb + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
                     if (!BWD) {

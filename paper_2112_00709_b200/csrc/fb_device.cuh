@@ -359,7 +359,7 @@ inline __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int
     const Graph &G = a.g;
     const size_t lat_base = (size_t)a.N_max * (G.G == 1 ? (size_t)b * K : (size_t)s0);
     for (int n = n0; n < n1; ++n) {
-        if (lattice && a.lat)
+        if (lattice && a.lat && !a.lat_int)  // a private lfmmi lattice is never read past N_b
             for (int j = tid; j < K; j += T) a.lat[lat_base + (size_t)n * K + j] = NEG_INF;
         if (lattice && a.scale && tid == 0) a.scale[(size_t)b * a.N_max + n] = 0.0;
         if (!bwd || a.post_kind == POST_NONE) continue;
