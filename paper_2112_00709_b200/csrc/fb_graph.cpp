@@ -1115,15 +1115,19 @@ extern "C" fb_status fb_graph_info(fb_graph h, int64_t *out) {
 
 extern "C" fb_status fb_graph_counters(fb_graph h, int64_t *out, int32_t reset) {
     if (!h || !out || h->g.dry) return FB_ERR_INVALID_ARG;
-    unsigned long long v[2] = {0, 0};
-    cudaError_t e = cudaMemcpy(v, h->g.ctr, sizeof v, cudaMemcpyDeviceToHost);  // synchronizes the device
-    if (e != cudaSuccess) { set_cuda_error("fb_graph_counters", (int)e); return FB_ERR_CUDA; }
-    out[0] = (int64_t)v[0];
-    out[1] = (int64_t)v[1];
-    if (reset) {
-        e = cudaMemset(h->g.ctr, 0, sizeof v);
-        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    // the handle's counters plus its relabelled twin's (lfmmi_loss_grad runs on the twin)
+    out[0] = out[1] = 0;
+    for (fb_graph x = h; x; x = x->perm) {
+        unsigned long long v[2] = {0, 0};
+        cudaError_t e = cudaMemcpy(v, x->g.ctr, sizeof v, cudaMemcpyDeviceToHost);  // synchronizes the device
         if (e != cudaSuccess) { set_cuda_error("fb_graph_counters", (int)e); return FB_ERR_CUDA; }
+        out[0] += (int64_t)v[0];
+        out[1] += (int64_t)v[1];
+        if (reset) {
+            e = cudaMemset(x->g.ctr, 0, sizeof v);
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { set_cuda_error("fb_graph_counters", (int)e); return FB_ERR_CUDA; }
+        }
     }
     return FB_OK;
 }
