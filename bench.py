@@ -142,6 +142,13 @@ def make_batch(rank: int, world: int = 1, mode: str = "c4"):
                       for _ in range(w.B)]
             w.emis = synth.emissions(rng, w.B, w.N_max, 84)
         return w
+    if mode == "c2":
+        # C2 (configs[1]): 64 left-to-right numerator graphs (G = B), N_b ~ U[max(120, L), 180], D = 300
+        w = synth.make_c2(seed=2)
+        if rank:
+            w.emis = synth.emissions(np.random.Generator(np.random.PCG64(2 + 1000 * rank)), w.B, w.N_max, w.D)
+        w.den = synth.compose(w.nums)  # the graph batch the public fb_forward / fb_backward calls take
+        return w
     if mode == "viterbi":
         return make_batch(rank, world, "c3")
     if mode == "viterbi-paper":
@@ -245,6 +252,7 @@ def ncu_traffic(args, n_launch: int):
         label = ("k_fbc" if kname.startswith("k_fbc") else "k_fb") + ("_bwd[G=1]" if "<true" in kname or "<1" in kname
                                                                       else "_fwd[G=1]")
         out.setdefault(label, d["bytes"])
+        out.setdefault(label.replace("[G=1]", "[G=B]"), d["bytes"])
     return out, "ncu (live: child process of this run, --metrics dram__bytes_read.sum,dram__bytes_write.sum)"
 
 
@@ -260,7 +268,7 @@ def ncu_child(args):
     den = fbx.Graph.from_host(w.den)
     emis = torch.from_numpy(w.emis).cuda()
     lens = torch.from_numpy(w.lengths).cuda()
-    if args.workload == "c3":
+    if args.workload in ("c3", "c2"):
         logZ, alpha, _, st = fbx.fb_forward(den, emis, lens)
         fbx.fb_backward(den, emis, lens, alpha=alpha, status=st)
     else:
@@ -286,7 +294,7 @@ def run_ours(args, rank, world, local):
     t0 = time.time()
     w = make_batch(rank, world, args.workload)
     Bw, Nw = w.B, w.N_max
-    c3 = args.workload == "c3"
+    c3 = args.workload in ("c3", "c2")  # public fb_forward + fb_backward (fused state posteriors)
     vit = args.workload.startswith("viterbi")
     num = None if (c3 or vit) else fbx.Graph.from_host(synth.compose(w.nums))
     den = fbx.Graph.from_host(w.den)
@@ -387,9 +395,10 @@ def run_ours(args, rank, world, local):
     # per-kernel roofline (dominant kernel: the denominator backward with the fused gradient epilogue)
     hbm, peak_src = measured_peaks()
     seq_frames = float(w.lengths.sum())
-    Dw, Kw = w.D, w.den.K
+    Kw = w.den.K if hasattr(w.den, "K") else w.den.K_tot / w.B  # C2: mean states per numerator graph
+    Dw = w.D if hasattr(w.den, "K") else min(w.D, Kw)          # C2: identity map, a graph reads K_b columns
     alg_bytes = {}  # algorithmic bytes per launch from the rank's true frames
-    bp_bytes = 2 if w.den.K <= 32767 else 4
+    bp_bytes = 2 if Kw <= 32767 else 4
     alg_bytes["k_viterbi"] = seq_frames * (4 * min(Dw, Kw) + bp_bytes * Kw)  # φ row (the columns read) + backpointer row
     for kname in ("k_fb", "k_fbc"):
         if c3:  # backward: φ row + α̂ row in, γ row out; forward: φ row in, α̂ row out
@@ -397,6 +406,9 @@ def run_ours(args, rank, world, local):
         else:   # backward: φ row + α̂ row in, grad row out; padded frames' grad rows are written 0 (fb.h)
             alg_bytes[kname + "_bwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw + 4 * Dw) + (Bw * Nw - seq_frames) * 4 * Dw
         alg_bytes[kname + "_fwd[G=1]"] = seq_frames * (4 * Dw + 4 * Kw)
+    for k in list(alg_bytes):  # per-sequence graph batches (C2) launch the same kernels as "[G=B]"
+        if k.endswith("[G=1]"):
+            alg_bytes[k.replace("[G=1]", "[G=B]")] = alg_bytes[k]
     kern = {}
     for name, (cnt, tot_ms) in prof.items():
         avg = tot_ms / max(cnt, 1)
@@ -411,6 +423,8 @@ def run_ours(args, rank, world, local):
                 "frac": (achieved / hbm) if achieved else None, "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg_bytes[dom]}
     step_bytes = alg_bytes["k_viterbi"] if vit else alg_bytes["k_fb_bwd[G=1]"] + alg_bytes["k_fb_fwd[G=1]"]
+    if args.workload == "c2":  # latency-bound: the per-frame step is the number to read
+        roofline["bound"] = "latency"
     den_kind = "k_fbc (cluster)" if den.info["cluster_C"] else "k_fb (one CTA per sequence)"
     launches = sum(c for c, _ in prof.values())
 
@@ -469,6 +483,8 @@ def run_ours(args, rank, world, local):
         "scaling": "strong" if args.workload == "c5-strong" else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded; SURVEY §8(d) recipes)",
         "config": {"workload": {"c4": WORKLOAD, "paper": WORKLOAD_N2, "c3": WORKLOAD_C3,
+                                "c2": "C2: 64 left-to-right numerator graphs (K 100-300, G = B), fb_forward + fb_backward "
+                                      "with state posteriors, φ[64,180,300], N_b ~ U[max(120, L), 180]",
                                 "viterbi": "N1: Viterbi (tropical semiring, fb_viterbi) over the C3 den, φ[128,500,3000]",
                                 "viterbi-paper": "N1: Viterbi over the paper's Table 1 den (3022 st / 50,984 arcs, "
                                                  "schedule streamed from L2), φ[128,700,84]"}.get(args.workload,
@@ -512,7 +528,7 @@ def main():
     ap.add_argument("--no-ncu", action="store_true", help="skip the live ncu DRAM-traffic capture (roofline.traffic)")
     ap.add_argument("--ncu-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--workload", default="c4",
-                    choices=["c4", "c3", "c5-weak", "c5-strong", "paper", "viterbi", "viterbi-paper"],
+                    choices=["c4", "c3", "c2", "c5-weak", "c5-strong", "paper", "viterbi", "viterbi-paper"],
                     help="c4 = the BASELINE metric config (default); c3 = den fwd+bwd+posteriors call sequence; "
                          "c5-* = variable-length 1024-utterance pool; paper = N2, the paper's Table 1 graph shape")
     args = ap.parse_args()

@@ -296,6 +296,26 @@ def test_viterbi_c3_den(fbx):
     _viterbi_check(fbx, w.den, w.emis, np.array([80, 13, 1, 55], np.int32))
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("which", ["c3", "paper"])
+def test_viterbi_full_size_sampled(fbx, which):
+    """N1 at the bench sizes (`bench.py --workload viterbi` / `viterbi-paper`: C3 den B=128, N=500;
+    the paper's den B=128, N=700, schedule streamed from L2) in the bench launch configuration;
+    the oracle recomputes sampled utterances — scores and paths bit for bit."""
+    import torch
+
+    w = synth.make_c3(seed=3) if which == "c3" else synth.make_paper_shape(seed=6)
+    g = fbx.Graph.from_host(w.den)
+    score, path, st = fbx.fb_viterbi(g, dev(w.emis), dev(w.lengths))
+    torch.cuda.synchronize()
+    assert (st.cpu().numpy() == 0).all()
+    score, path = score.cpu().numpy(), path.cpu().numpy()
+    for b in (0, 63, 127):
+        ref = oracle.viterbi_batch(w.den, w.emis[b:b + 1], w.lengths[b:b + 1])
+        assert score[b] == ref["score"][0]
+        assert (path[b] == ref["path"][0]).all()
+
+
 def test_viterbi_paper_shape_n2(fbx):
     """N1 on the paper's Table 1 denominator (3022 states, 50,984 arcs): its
     float64 Viterbi schedule exceeds shared memory and is streamed from global memory
