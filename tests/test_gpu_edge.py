@@ -360,7 +360,7 @@ def test_n3_forced_factored_tight_numerators(fbx, kind):
     assert (ref["status"] == 0).all() and (st2.cpu().numpy() == 0).all()
     assert logz_err(logZ.cpu().numpy(), ref["logZ"], np.ones(16, bool)) <= TOL_LOGZ
     assert logz_err(logZb.cpu().numpy(), ref["logZ"], np.ones(16, bool)) <= TOL_LOGZ
-    tol = TOL_POST if kind != "softmax8" else 3 * TOL_POST  # σ = 8: reported stress case
+    tol = TOL_POST  # σ = 8 included: measured within the primary gate (profiles/r2_parity_errors.txt)
     assert np.abs(post.cpu().numpy() - ref["post"]).max() <= tol
     # the exact max-then-sum fallback of the factored ⊕ ran on these inputs
     assert ctr["fallback_rows"] > 0, ctr
@@ -378,7 +378,7 @@ def test_n3_den_sigma8_factored_vs_exact(fbx):
         assert (r["st"] == 0).all()
         assert logz_err(r["logZ"], ref["logZ"], np.ones(4, bool)) <= TOL_LOGZ
         errs[flags] = np.abs(r["post"].reshape(ref["post"].shape) - ref["post"]).max()
-    assert max(errs.values()) <= 3 * TOL_POST, errs
+    assert max(errs.values()) <= TOL_POST, errs  # measured 2.4e-6 (profiles/r2_parity_errors.txt)
 
 
 @pytest.mark.parametrize("flags", [0, 1, 2])

@@ -112,7 +112,7 @@ def test_c3_den_reduced(fbx, kind, flags, K, nnz):
     assert (r["st"] == 0).all()
     check_logZ(r["logZ"], ref["logZ"], np.ones(6, bool))
     err = np.abs(r["post"].reshape(ref["post"].shape) - ref["post"]).max()
-    tol = TOL_POST if kind != "softmax8" else 3 * TOL_POST  # σ = 8 is a reported stress case
+    tol = TOL_POST  # σ = 8 too: measured 2.4e-6 on the den (profiles/r2_parity_errors.txt)
     assert err <= tol, err
     # posteriors sum to 1 on valid frames, 0 on padding
     P = r["post"].reshape(6, 64, -1)
