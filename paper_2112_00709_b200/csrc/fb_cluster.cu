@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     constexpr float kTiny = 8.271806125530277e-25f, kHuge = 1.329227995784916e+36f;  // 2^-80, 2^120
     const Graph &G = a.g;
     const CPlan &P = G.cp;
+    const bool SPLIT = (P.split >> (BWD ? 1 : 0)) & 1;  // this direction's phase A is split around the wait
     const int C = P.C;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int cr = (int)cl_rank();
@@ -284,8 +285,8 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 
     // ---- schedule and pdf map → shared memory; mbarriers
     {
-        const int m0 = P.split ? 2 * cr : cr;  // split: members 2c, 2c+1 back to back
-        for (int m = m0; m <= (P.split ? m0 + 1 : m0); ++m) {
+        const int m0 = SPLIT ? 2 * cr : cr;  // split: members 2c, 2c+1 back to back
+        for (int m = m0; m <= (SPLIT ? m0 + 1 : m0); ++m) {
             const uint4 *src = (const uint4 *)(SC.rec + SC.rec_off[m]);
             uint4 *dst = (uint4 *)(smem_raw + L.rec + (m > m0 ? SC.rec_bytes[m0] : 0));
             const int n16 = SC.rec_bytes[m] >> 4;
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     }
 
     // ---- frames 1 … Tmax−1 (+ one flush step t = Tmax for the last posterior rows)
-    const int split = P.split;
+    const int split = SPLIT;
     const int mr = split ? 2 * cr + 1 : cr;  // remote-source (or whole) member
     const int nsl = SC.warp_nsl[mr * W + warp];
     const uint32_t mysl = a_rec + (uint32_t)(split ? SC.rec_bytes[2 * cr] : 0) + (uint32_t)SC.warp_off[mr * W + warp];

@@ -361,8 +361,11 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
     // local/remote split of phase A around the exchange wait: measured faster for the
     // no-p (4,4) paper-shape plan (N2 fwd 5.36 → 5.12 ms, bwd 8.72 → 8.36 ms), slower
     // for (2,2) on C3/C4 (6.52 → 6.94 ms); FBX_CLUSTER_SPLIT=0|1 overrides
-    cp.split = nop ? 1 : 0;
-    if (const char *e = std::getenv("FBX_CLUSTER_SPLIT")) cp.split = std::atoi(e) != 0;
+    // bit 0: forward, bit 1: backward.  With p-exchange (round 2) the forward is faster
+    // unsplit (N2 3.72 → 3.60 ms) while the backward keeps the split (5.73 vs 5.77 ms).
+    cp.split = nop ? 2 : 0;
+    if (const char *e = std::getenv("FBX_CLUSTER_SPLIT"))  // 0 none, 1 both, f forward only, b backward only
+        cp.split = e[0] == 'f' ? 1 : e[0] == 'b' ? 2 : (std::atoi(e) != 0 ? 3 : 0);
     std::vector<double> cost(D, 0.0);
     for (int k = 0; k < K; ++k)
         cost[pdf[k]] += (in.ptr[k + 1] - in.ptr[k]) + (out.ptr[k + 1] - out.ptr[k]) + 8.0;
@@ -452,11 +455,12 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
     for (int dir = 0; dir < 2; ++dir) {
         const RowLists &rl = dir ? out : in;
         HostSched &hs = dir ? cp.hb : cp.hf;
+        const bool sp = (cp.split >> dir) & 1;
         for (int c = 0; c < C; ++c) {
             const int Kc = cp.part_off[c + 1] - cp.part_off[c];
             // split: member 2c = arcs from this part's own states (run before the
             // exchange wait), member 2c+1 = arcs from the other parts
-            for (int pass = 0; pass < (cp.split ? 2 : 1); ++pass) {
+            for (int pass = 0; pass < (sp ? 2 : 1); ++pass) {
                 RowLists pl;
                 pl.ptr.assign(Kc + 1, 0);
                 for (int r = 0; r < Kc; ++r) {
@@ -465,7 +469,7 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
                         for (int a = rl.ptr[o]; a < rl.ptr[o + 1]; ++a) {
                             const int si = inv[rl.other[a]];
                             const bool local = si >= cp.part_off[c] && si < cp.part_off[c + 1];
-                            if (cp.split && local != (pass == 0)) continue;
+                            if (sp && local != (pass == 0)) continue;
                             pl.other.push_back(si);
                             pl.w.push_back(rl.w[a]);
                         }
@@ -474,7 +478,7 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
                 if (!build_member_sched(pl, Kc, T, MODE_FACTORED, 4 * S, Lmax, hs, true)) return false;
             }
         }
-        if (cp.split) {  // both members of a part sit back to back in shared memory
+        if (sp) {  // both members of a part sit back to back in shared memory
             hs.bytes_max = 0;
             for (int c = 0; c < C; ++c) hs.bytes_max = std::max(hs.bytes_max, hs.rec_bytes[2 * c] + hs.rec_bytes[2 * c + 1]);
         }

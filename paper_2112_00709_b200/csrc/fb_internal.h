@@ -75,8 +75,9 @@ struct PdfMap {
 struct CPlan {
     int ok = 0, C = 0, S = 0, T = 0, spt = 0, K_int = 0, Kc_max = 0, Dc_max = 0;
     int nop = 0;                        // no p = 2^u array: phase A applies ex2 to the gathered u (smem-bound configs)
-    int split = 0;                      // members 2c / 2c+1: part c's local-source / remote-source arcs (phase A
-                                        // split around the exchange wait); else member c = all of part c's arcs
+    int split = 0;                      // bit 0 forward, bit 1 backward: members 2c / 2c+1 = part c's local-source /
+                                        // remote-source arcs (phase A split around the exchange wait); else member
+                                        // c = all of part c's arcs
     int emis16 = 0;                     // emission segments are 16-byte aligned (D % 4 == 0)
     const int *part_off = nullptr;      // [C+1] internal state offsets
     const int *pdf_lo = nullptr;        // [C+1] part c owns pdfs [pdf_lo[c], pdf_lo[c+1])
