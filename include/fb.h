@@ -279,6 +279,20 @@ fb_status fb_forward_literal(fb_graph g, int32_t semiring, const float *log_emis
                              void *stream);
 
 /*
+ * fb_forward_semiring — the fused one-CTA-per-sequence forward of Eq. (13)
+ * instantiated for any of the three semirings (SURVEY
+ * §8(f) N4): score[b] = ⊕ over accepting paths of π ⊗ Π v ⊗ Π T ⊗ ω, float64,
+ * no normalisation — FB_SEMIRING_LOG: log Z_b (= fb_forward's logZ);
+ * FB_SEMIRING_TROPICAL: the best-path score (= fb_viterbi's score);
+ * FB_SEMIRING_PROB: Z_b in the linear domain (0 where it underflows, P:93-96;
+ * the sequence is then flagged FB_SEQ_EMPTY_LATTICE like a true 0̄).  Same arc
+ * schedule and per-frame phases as the tuned kernels; seq_status as fb_forward.
+ * FB_ERR_UNSUPPORTED for member graphs over 8192 states.
+ */
+fb_status fb_forward_semiring(fb_graph g, int32_t semiring, const float *log_emis, const int32_t *lengths,
+                              int32_t B, int32_t N_max, double *score, int32_t *seq_status, void *stream);
+
+/*
  * fb_forward_backward_literal — the literal strategy's full forward-backward
  * (SURVEY §8(f) N4): fb_forward_literal's forward storing every frame's batch
  * vector X_n, then the backward of the same block-diagonal matrix, one SpMV per

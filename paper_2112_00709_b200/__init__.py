@@ -25,7 +25,7 @@ from ._lib import EXPORTS, lib  # noqa: F401
 
 __all__ = [
     "FBError", "Graph", "fb_forward", "fb_backward", "fb_posteriors", "fb_gap", "lfmmi_loss_grad", "workspace_bytes",
-    "fb_viterbi", "fb_forward_literal", "fb_forward_backward_literal", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
+    "fb_viterbi", "fb_forward_semiring", "fb_forward_literal", "fb_forward_backward_literal", "lfmmi_loss_grad_host", "profile_enable", "profile_reset", "profile_collect",
     "SEMIRING_LOG", "SEMIRING_TROPICAL", "SEMIRING_PROB",
     "SEQ_OK", "SEQ_EMPTY_LATTICE", "SEQ_NONFINITE_INPUT", "SEQ_BAD_LENGTH",
     "GRAPH_DEFAULT", "GRAPH_FORCE_EXACT", "GRAPH_FORCE_FACTORED", "GRAPH_CLUSTER",
@@ -377,6 +377,21 @@ def fb_forward_literal(g: Graph, emis, lengths, semiring: int = SEMIRING_LOG):
                                     _dev(score, torch.float64, "score"), _dev(ws, torch.uint8, "workspace"),
                                     ws.numel(), _stream()), "fb_forward_literal")
     return score
+
+
+def fb_forward_semiring(g: Graph, emis, lengths, semiring: int = SEMIRING_LOG):
+    """The fused forward (Eq. (13)) in the log / tropical / probability semiring (N4).
+    Returns (score [B] f64, status [B] i32)."""
+    import torch
+
+    B, N_max, D = _check_inputs(g, emis, lengths, "fb_forward_semiring")
+    dev = emis.device
+    score = torch.empty(B, dtype=torch.float64, device=dev)
+    st = torch.empty(B, dtype=torch.int32, device=dev)
+    _check(lib().fb_forward_semiring(g.handle, int(semiring), _dev(emis, torch.float32, "emis"),
+                                     _dev(lengths, torch.int32, "lengths"), B, N_max, _dev(score, torch.float64, "score"),
+                                     _dev(st, torch.int32, "status"), _stream()), "fb_forward_semiring")
+    return score, st
 
 
 def fb_forward_backward_literal(g: Graph, emis, lengths, semiring: int = SEMIRING_LOG, want_post: bool = True):

@@ -32,6 +32,7 @@ _SIGS = {
     "fb_viterbi": (c_i32, [c_p, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_p, c_sz, c_p]),
     "fb_literal_workspace_bytes": (c_sz, [c_p, c_i32]),
     "fb_forward_literal": (c_i32, [c_p, c_i32, c_p, c_p, c_i32, c_i32, c_p, c_p, c_sz, c_p]),
+    "fb_forward_semiring": (c_i32, [c_p, c_i32, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p]),
     "fb_literal_fb_workspace_bytes": (c_sz, [c_p, c_i32, c_i32]),
     "fb_forward_backward_literal": (c_i32, [c_p, c_i32, c_p, c_p, c_i32, c_i32, c_p, c_p, c_p, c_sz, c_p]),
     "fb_profile_enable": (None, [c_i32]),

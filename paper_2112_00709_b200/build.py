@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("FBX_LIB_OUT") or os.path.join(HERE, "libfb.so")  # FBX_LIB_OUT: experiment builds
 EXTRA = os.environ.get("FBX_EXTRA_FLAGS", "").split()  # e.g. -DFBX_CTIMING (instrumented experiment builds)
 OBJ_TAG = os.environ.get("FBX_OBJ_TAG", "")
-SOURCES = ["fb_graph.cpp", "fb_kernels.cu", "fb_inst.cu", "fb_cluster.cu", "fb_literal.cu"]
+SOURCES = ["fb_graph.cpp", "fb_kernels.cu", "fb_inst.cu", "fb_cluster.cu", "fb_literal.cu", "fb_semiring.cu"]
 # fb_inst.cu is compiled once per (direction, mode): the k_fb instantiation sets
 INST = [(bwd, mode) for bwd in (0, 1) for mode in (0, 1, 2, 4)]
 # fb_cluster.cu once per (direction, sequences per cluster)
@@ -39,7 +39,7 @@ def _units():
     units = [("fb_graph.cpp", "fb_graph.o", []), ("fb_kernels.cu", "fb_kernels.o", [])]
     units += [("fb_inst.cu", f"fb_inst_b{b}_m{m}.o", [f"-DFBX_BWD={b}", f"-DFBX_MODE={m}"]) for b, m in INST]
     units += [("fb_cluster.cu", f"fb_cluster_b{b}_s{s}.o", [f"-DFBX_BWD={b}", f"-DFBX_S={s}"]) for b, s in CINST]
-    units += [("fb_literal.cu", "fb_literal.o", [])]
+    units += [("fb_literal.cu", "fb_literal.o", []), ("fb_semiring.cu", "fb_semiring.o", [])]
     return units
 
 

@@ -183,3 +183,74 @@ def test_literal_fb_prob_and_tropical(fbx):
         path = vit["path"][b, : lens[b]]
         assert np.abs(P[np.arange(lens[b]), path] - 1).max() <= 1e-9
     torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ fused semiring-generic forward (N4)
+
+@pytest.mark.parametrize("which", ["c1", "small", "c2", "c3", "n2"])
+def test_fused_forward_semirings(fbx, which):
+    """fb_forward_semiring: one fused kernel body instantiated for the log, tropical and
+    probability semirings.  Log = the oracle's log Z, tropical = the oracle's
+    Viterbi score, probability = exp(log Z) where it does not underflow; numerator batches
+    (G = B), the irregular brute-force family, a shared den (G = 1) and the paper's den
+    (schedule streamed from L2)."""
+    import torch
+
+    if which == "c1":
+        ws = [synth.make_c1(s) for s in range(40)]
+        g = synth.compose([w.den for w in ws])
+        emis = np.concatenate([w.emis for w in ws])
+        lens = np.full(40, 6, np.int32)
+        lens[::5] = 2
+    elif which == "small":
+        rng = np.random.Generator(np.random.PCG64(88))
+        gs = [synth.random_small_graph(rng, K=int(rng.integers(1, 7)), D=6) for _ in range(60)]
+        g = synth.compose(gs)
+        emis = rng.uniform(-3, 0, (60, 7, 6)).astype(np.float32)
+        lens = rng.integers(1, 8, 60).astype(np.int32)
+    elif which == "c2":
+        w = synth.make_c2(seed=8, B=8)
+        g, emis, lens = synth.compose(w.nums), w.emis, w.lengths
+    elif which == "c3":
+        w = synth.make_c3(seed=36, B=3, N=40, K=3000, nnz=20000)
+        g, emis, lens = w.den, w.emis, np.array([40, 17, 40], np.int32)
+    else:
+        w = synth.make_paper_shape(seed=6, B=2, N=30, L_range=(5, 10))
+        g, emis, lens = w.den, w.emis, np.array([30, 21], np.int32)
+    G = fbx.Graph.from_host(g)
+    e, L = dev(emis), dev(lens)
+    out = {sr: fbx.fb_forward_semiring(G, e, L, sr) for sr in (fbx.SEMIRING_LOG, fbx.SEMIRING_TROPICAL,
+                                                                fbx.SEMIRING_PROB)}
+    torch.cuda.synchronize()
+    ref = oracle.fb_batch(g, emis, lens, post=False)
+    vit = oracle.viterbi_batch(g, emis, lens)
+    ok = ref["status"] == 0
+    zl, stl = (x.cpu().numpy() for x in out[fbx.SEMIRING_LOG])
+    assert (stl == ref["status"]).all()
+    assert np.abs(zl[ok] - ref["logZ"][ok]).max(initial=0) <= 1e-12 * max(1.0, np.abs(ref["logZ"][ok]).max(initial=1))
+    zt, stt = (x.cpu().numpy() for x in out[fbx.SEMIRING_TROPICAL])
+    assert (stt == vit["status"]).all()
+    okv = vit["status"] == 0
+    assert np.abs(zt[okv] - vit["score"][okv]).max(initial=0) <= 1e-12 * max(1.0, np.abs(vit["score"][okv]).max(initial=1))
+    zp, stp = (x.cpu().numpy() for x in out[fbx.SEMIRING_PROB])
+    lin = np.exp(ref["logZ"])
+    fine = ok & (lin > 1e-280)
+    assert (np.abs(zp[fine] - lin[fine]) / lin[fine]).max(initial=0) <= 1e-11
+    assert (zp[ok & (lin == 0)] == 0).all() and (stp[ok & (lin == 0)] == fbx.SEQ_EMPTY_LATTICE).all()
+
+
+def test_fused_prob_semiring_underflows_on_ac6(fbx):
+    """AC6: the fused probability instance returns exactly 0 (flagged as an empty
+    lattice) while the log instance matches the oracle's finite log Z."""
+    import torch
+
+    lr = helpers.left_to_right(10)
+    e = np.random.default_rng(6).uniform(-100, -50, (1, 1000, 10)).astype(np.float32)
+    L = np.array([1000], np.int32)
+    G = fbx.Graph.from_host(lr)
+    zp, sp = fbx.fb_forward_semiring(G, dev(e), dev(L), fbx.SEMIRING_PROB)
+    zl, sl = fbx.fb_forward_semiring(G, dev(e), dev(L), fbx.SEMIRING_LOG)
+    torch.cuda.synchronize()
+    ref = oracle.fb_batch(lr, e, L, post=False)["logZ"][0]
+    assert zp.item() == 0.0 and sp.item() == fbx.SEQ_EMPTY_LATTICE
+    assert sl.item() == 0 and abs(zl.item() - ref) <= 1e-12 * abs(ref)
