@@ -440,7 +440,8 @@ def run_ours(args, rank, world, local):
         k2 = max(3, min(args.steps, 10))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        bufs["copy_stream"].wait_event(e0)  # the first upload starts inside the timed region
+        for cs_ in bufs["copy_streams"]:
+            cs_.wait_event(e0)  # the first upload starts inside the timed region
         for _ in range(k2):
             out = fbx.lfmmi_loss_grad_host(num, den, emis_h, lens_h, bufs)
             if world > 1:
