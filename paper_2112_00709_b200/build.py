@@ -18,7 +18,7 @@ EXTRA = os.environ.get("FBX_EXTRA_FLAGS", "").split()  # e.g. -DFBX_CTIMING (ins
 OBJ_TAG = os.environ.get("FBX_OBJ_TAG", "")
 SOURCES = ["fb_graph.cpp", "fb_kernels.cu", "fb_inst.cu", "fb_cluster.cu", "fb_literal.cu", "fb_semiring.cu"]
 # fb_inst.cu is compiled once per (direction, mode): the k_fb instantiation sets
-INST = [(bwd, mode) for bwd in (0, 1) for mode in (0, 1, 2, 4)]
+INST = [(bwd, mode) for bwd in (0, 1) for mode in (0, 1, 2, 4)] + [(1, 5)]
 # fb_cluster.cu once per (direction, sequences per cluster)
 CINST = [(bwd, s) for bwd in (0, 1) for s in (2, 4)]
 HEADERS = ["fb_internal.h", "fb_device.cuh", os.path.join("..", "..", "include", "fb.h")]

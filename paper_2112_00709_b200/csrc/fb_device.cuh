@@ -193,6 +193,11 @@ struct FBArgs {
     double *lat64;
     const double *alpha64;
     const double *logZ_in;
+    // kModeGradIZ (lfmmi den backward): the forward's per-frame offsets C_n (natural log,
+    // [B][N_max]) and log Z, so the posterior normaliser of frame n is known up front:
+    // Ẑ_n = log Z − C_n − D_n (Eq. (1) invariant)
+    const double *ascale_in;
+    const double *logZ_fwd;
 };
 
 // Exact max-then-sum over one row held by g lanes (fallback of factored mode,
@@ -316,7 +321,7 @@ __device__ __forceinline__ int lds_s16(uint32_t a) {
     return (int)v;
 }
 __device__ __forceinline__ void pdf_row(const FBArgs &a, uint32_t a_gbuf, uint32_t a_ssp, uint32_t a_pq, int gi,
-                                        int b, int n, int tid, int T) {
+                                        int b, int n, int tid, int T, float mul) {
     const Graph &G = a.g;
     const PdfMap &pm = G.pm;
     if (a.post_kind == POST_PDF_COMPACT) {
@@ -333,7 +338,9 @@ __device__ __forceinline__ void pdf_row(const FBArgs &a, uint32_t a_gbuf, uint32
     // dense / grad: pdf d sums its run gbuf[q0, q0 + count) of pq[d]
     const int D = a.D;
     float *row = a.post + ((size_t)b * a.N_max + n) * D;
-    const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;  // grad: −Γ_den; Γ_num added by k_add_num
+    // mul: +1 (posteriors), −1 (grad: −Γ_den; Γ_num added by k_add_num), or −1/S when gbuf
+    // holds unnormalised e = γ·S (kModeGradIZ)
+    const float sgn = mul;
     auto run = [&](uint32_t w) {
         const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
         float acc = 0.f;
@@ -361,7 +368,7 @@ inline __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int
     for (int n = n0; n < n1; ++n) {
         if (lattice && a.lat && !a.lat_int)  // a private lfmmi lattice is never read past N_b
             for (int j = tid; j < K; j += T) a.lat[lat_base + (size_t)n * K + j] = NEG_INF;
-        if (lattice && a.scale && tid == 0) a.scale[(size_t)b * a.N_max + n] = 0.0;
+        if (lattice && a.scale && !a.lat_int && tid == 0) a.scale[(size_t)b * a.N_max + n] = 0.0;
         if (!bwd || a.post_kind == POST_NONE) continue;
         if (a.post_kind == POST_STATE) {
             for (int j = tid; j < K; j += T) a.post[lat_base + (size_t)n * K + j] = 0.f;
@@ -384,11 +391,25 @@ inline __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int
 // frame is the one-frame change of the recursion, so exp2 of the vector stays
 // in range (exact fallback otherwise).
 // MODEX: MODE_FACTORED / MODE_EXACT / MODE_RAW, or kModeFactoredTma (factored
-// arithmetic with φ rows staged through TMA).
+// arithmetic with φ rows staged through TMA), or kModeGradIZ (the same, backward
+// with the −Γ_den gradient epilogue normalised through the forward's log Z).
+//
+// kModeGradIZ epilogue.  By Eq. (1) Σ_k α_n(k) β_n(k) = Z at every n, so in
+// the normalised log2 units of the kernels the posterior normaliser of frame n is
+// Ẑ_n = log2 Z − C_n − D_n, known before the frame is computed (C_n: the forward's
+// offsets, D_n: this pass's).  Phase B then forms e_k = 2^{α̂_n(k) + β̂_n(k) − Ẑ_n}
+// (one ex2 per state) straight into the γ buffer and sums it per warp; the next
+// frame's phase A sums the 32 partials (every warp redundantly: no extra barrier)
+// and writes the gradient row −Σ_{k∈pdf} e_k / S.  Dividing by the computed
+// S = Σ_k e_k (≈ 1, off by the float32 rounding of the two recursions) keeps
+// Σ_k γ_n(k) = 1 exactly as the two-pass max-then-sum normaliser did; it replaces
+// that pass's per-state max reduction and second ex2, and the one-frame lag of γ.
 constexpr int kModeFactoredTma = 4;
+constexpr int kModeGradIZ = 5;
 template <bool BWD, int MODEX, int SPT, int TT>
 __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
-    constexpr bool TMA = MODEX == kModeFactoredTma;
+    constexpr bool IZ = BWD && MODEX == kModeGradIZ;
+    constexpr bool TMA = MODEX == kModeFactoredTma || MODEX == kModeGradIZ;
     constexpr int MODE = TMA ? (int)MODE_FACTORED : MODEX;
     using V = typename std::conditional<MODE == MODE_FACTORED, float, double>::type;
     constexpr uint32_t VS = sizeof(V);
@@ -402,8 +423,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     const int K = G.state_off[gi + 1] - s0;
     const int N = a.lengths[b];
     const Sched &S = BWD ? G.bwd : G.fwd;
-    const bool want_post = BWD && a.post_kind != POST_NONE;
-    const bool pdf_post = want_post && a.post_kind != POST_STATE;
+    const bool want_post = IZ || (BWD && a.post_kind != POST_NONE);
+    const bool pdf_post = IZ || (want_post && a.post_kind != POST_STATE);
     const SmemLayout SL = smem_layout(S.bytes_max, T * SPT, MODE != MODE_FACTORED, want_post && pdf_post);
     const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t a_u = sb + (uint32_t)SL.u, a_p = sb + (uint32_t)SL.p, a_part = sb + (uint32_t)SL.part;
@@ -551,7 +572,13 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     float vA[SPT], vB[SPT];  // emissions
     V aA[SPT], aB[SPT];      // α̂ (backward epilogue), log2 units
     V uk[SPT];               // this thread's entries of the current vector u (log2)
-    V xpost[SPT];            // α̂_n + β̂_n of the frame whose posterior is pending
+    V xpost[SPT];            // α̂_n + β̂_n of the frame whose posterior is pending (not IZ)
+    double scale = 0.0;      // C_n (fwd) / D_n (bwd), log2 units
+    const float psgn = a.post_kind == POST_GRAD ? -1.f : 1.f;
+    // IZ: log2 Z of the forward, and the normaliser Ẑ of the frame being emitted
+    const double logZ2 = IZ ? a.logZ_fwd[b] * 1.4426950408889634 : 0.0;
+    float zhat = 0.f;
+    auto zhat_of = [&](double cn_nat) { return (float)(logZ2 - cn_nat * 1.4426950408889634 - scale); };
     const int dir = BWD ? -1 : 1;
     const int n_first = BWD ? N - 1 : 0;
     load_v(n_first, vA);
@@ -560,7 +587,6 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     tma_issue(1, n_first + dir);
     int tstep = 0;  // index of the frame being produced (t in tma_issue / fetch_v)
     if (want_post) { load_alpha(n_first, aA); load_alpha(n_first + dir, aB); }
-    double scale = 0.0;  // C_n (fwd) / D_n (bwd), log2 units
     float vsum = 0.f;    // Σ of every emission read: NaN / +∞ ⇒ non-finite input
     int par = 0;         // parity of the reduction buffers of the current frame
 
@@ -583,12 +609,23 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
             lmax = warp_max_fast(lmax);
             if (lane == 0) sts_v(a_wmax + (uint32_t)(par * 32 + warp) * 8, lmax);
         }
-        if (want_post) {
+        if (IZ) {  // e_k = 2^{α̂ + β̂ − Ẑ_n} into the γ buffer; per-warp Σ e
+            float es = 0.f;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                const float e = ex2((float)(acur[k] * L2E + h[k]) - zhat);  // 0 for non-viable / inert
+                if (tid + k * T < K) sts_v(a_gbuf + 4 * (uint32_t)posk[k], e);
+                es += e;
+            }
+            es = warp_sum(es);
+            if (lane == 0) sts_v(a_wz + (uint32_t)(par * 64 + warp) * 8, es);
+        }
+        if (want_post && !IZ) {
 #pragma unroll
             for (int k = 0; k < SPT; ++k)
                 xpost[k] = (tid + k * T < K) ? (RAW ? acur[k] : acur[k] * L2E) + h[k] : NINF;
         }
-        if (want_post && !RAW) {
+        if (want_post && !RAW && !IZ) {
             V zm;
             float zs;
             warp_lse_vals<V, SPT>(xpost, zm, zs);
@@ -629,6 +666,12 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
             }
         }
     };
+    auto iz_row = [&](int pn, int pp) {
+        float sv = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + lane) * 8, 0.f) : 0.f;
+        sv = warp_sum(sv);  // every warp the same S (same partials, same order)
+        const float mul = (sv > 0.f && sv < INFINITY) ? -1.f / sv : 0.f;
+        pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pn, tid, T, mul);
+    };
     auto block_max_prev = [&](int pp) {
         const V v = lane < W ? lds_v(a_wmax + (uint32_t)(pp * 32 + lane) * 8, (V)0) : NINF;
         return warp_max_fast(v);
@@ -667,6 +710,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k) { h[k] -= c; uk[k] -= c; }
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n_first] = scale * kLN2;
+        if (IZ) zhat = zhat_of(a.ascale_in[(size_t)b * a.N_max + n_first]);
         emit(n_first, h, aA);
         load_v(n_first + 2 * dir, vA);
         if (want_post) load_alpha(n_first + 2 * dir, aA);
@@ -679,10 +723,12 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         __syncthreads();  // u, p, wmax[par], wz[par] of frame n visible
         ++tstep;
         tma_issue(tstep + 1, n_next + dir);  // buffer of step tstep-1 is free now
+        double cn_next = 0.0;  // IZ: the forward's C of frame n_next (used in phase B)
+        if (IZ) cn_next = __ldg(a.ascale_in + (size_t)b * a.N_max + n_next);
         if (!RAW && warp == 0) {  // the frame's normaliser c and posterior Z, reduced once (read after the next barrier)
             const V cmax = block_max_prev(par);
             V Zr = (V)0;
-            if (want_post) {
+            if (want_post && !IZ) {
                 const V m = lane < W ? lds_v(a_wz + (uint32_t)(par * 64 + 2 * lane) * 8, (V)0) : NINF;
                 const float s2 = lane < W ? lds_v(a_wz + (uint32_t)(par * 64 + 2 * lane + 1) * 8, 0.f) : 0.f;
                 Zr = block_lse_pairs<V>(m, s2);
@@ -693,19 +739,21 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
             }
         }
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
-        if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T);
+        if (IZ) iz_row(n, par);  // gradient row of frame n (its e in gbuf, partials in wz[par])
+        else if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T, psgn);
         phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part, G.ctr);
         __syncthreads();
         // ---- phase B of frame n_next
         const int pp = par;
         par ^= 1;
-        if (want_post) posterior(n, pp, true);  // γ_n (its x is in registers, Z in cz[pp])
+        if (want_post && !IZ) posterior(n, pp, true);  // γ_n (its x is in registers, Z in cz[pp])
         pend_n = n;
         n = n_next;
         V c = RAW ? (V)0 : lds_v(a_cz + (uint32_t)(2 * pp) * 8, (V)0);  // lagged normaliser: max of the previous u
         if (c == NINF) c = (V)0;                // no viable state: keep 0̄ everywhere
         scale += (double)c;
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
+        if (IZ) zhat = zhat_of(cn_next);
         V h[SPT];
         float vv[SPT];
         fetch_v(tstep, vb, vv);
@@ -734,14 +782,17 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         if (!step(vA, aA)) break;
     }
     // ---- flush the pending posterior rows
-    if (want_post) {
+    if (IZ) {
+        __syncthreads();  // gbuf and wz[par] of the last frame visible
+        iz_row(n, par);
+    } else if (want_post) {
         __syncthreads();  // wz[par] of the last frame visible; gbuf of pend_n complete
-        if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T);
+        if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T, psgn);
         if (pdf_post) __syncthreads();  // gbuf free again
         posterior(n, par, false);
         if (pdf_post) {
             __syncthreads();
-            pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, n, tid, T);
+            pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, n, tid, T, psgn);
         }
     }
     // ---- termination: logZ = C + ⊕_k α̂(k) ⊗ ω(k)  /  logZ_β = D_0 + ⊕_k π(k) ⊗ u_0(k)
@@ -833,6 +884,7 @@ KFn pick_fb(int spt, int T);
 #define FBX_PICK_EXTERN(B, M) extern template KFn pick_fb<B, M>(int, int);
 FBX_PICK_EXTERN(false, 0) FBX_PICK_EXTERN(false, 1) FBX_PICK_EXTERN(false, 2) FBX_PICK_EXTERN(false, 4)
 FBX_PICK_EXTERN(true, 0) FBX_PICK_EXTERN(true, 1) FBX_PICK_EXTERN(true, 2) FBX_PICK_EXTERN(true, 4)
+FBX_PICK_EXTERN(true, 5)
 #undef FBX_PICK_EXTERN
 
 }  // namespace fbx

@@ -457,6 +457,7 @@ __global__ void k_totals(const double *zn, const double *zd, const int *lengths,
 
 static KFn pick(bool bwd, int mode, int spt, int T) {
     if (bwd) {
+        if (mode == kModeGradIZ) return pick_fb<true, kModeGradIZ>(spt, T);
         if (mode == kModeFactoredTma) return pick_fb<true, kModeFactoredTma>(spt, T);
         if (mode == MODE_FACTORED) return pick_fb<true, MODE_FACTORED>(spt, T);
         if (mode == MODE_RAW) return pick_fb<true, MODE_RAW>(spt, T);
@@ -602,7 +603,9 @@ static fb_status launch_fb(bool bwd, const FBArgs &a, cudaStream_t s, bool raw =
     aa.tma = G.mode == MODE_FACTORED && !raw && (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0) &&
              sm + tma_bytes <= (size_t)kSmemLimit && std::getenv("FBX_NO_TMA") == nullptr;
     if (aa.tma) sm += tma_bytes;
-    KFn fn = pick(bwd, raw ? (int)MODE_RAW : (aa.tma ? kModeFactoredTma : G.mode), G.spt, G.T);
+    // the lfmmi den backward normalises γ through the forward's log Z (kModeGradIZ, fb_device.cuh)
+    const bool iz = bwd && aa.tma && a.post_kind == POST_GRAD && a.ascale_in && a.logZ_fwd;
+    KFn fn = pick(bwd, raw ? (int)MODE_RAW : (iz ? kModeGradIZ : (aa.tma ? kModeFactoredTma : G.mode)), G.spt, G.T);
     if (fb_status r0 = set_smem((const void *)fn, sm); r0 != FB_OK) return r0;
     {
         ProfScope ps(bwd ? (G.G == 1 ? "k_fb_bwd[G=1]" : "k_fb_bwd[G=B]") : (G.G == 1 ? "k_fb_fwd[G=1]" : "k_fb_fwd[G=B]"), s);
@@ -675,7 +678,7 @@ static int sm_count(int dev) {
 }
 
 struct WsLayout {
-    size_t den_alpha, num_alpha, gnum, zn, zd, nst, total;
+    size_t den_alpha, num_alpha, gnum, zn, zd, nst, den_scale, total;
 };
 static size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
 static WsLayout ws_layout(const Graph &num, const Graph &den, int B, int N_max) {
@@ -688,6 +691,7 @@ static WsLayout ws_layout(const Graph &num, const Graph &den, int B, int N_max) 
     w.zn = o; o += a256((size_t)B * 8);
     w.zd = o; o += a256((size_t)B * 8);
     w.nst = o; o += a256((size_t)B * 4);
+    w.den_scale = o; o += a256((size_t)B * N_max * 8);  // the den forward's per-frame offsets C_n
     w.total = o;
     return w;
 }
@@ -790,6 +794,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     float *gnum = (float *)(ws + L.gnum);
     double *zn = (double *)(ws + L.zn), *zd = (double *)(ws + L.zd);
     int *nst = (int *)(ws + L.nst);
+    double *den_scale = (double *)(ws + L.den_scale);
     cudaStream_t s = (cudaStream_t)stream;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return FB_ERR_CUDA;
@@ -805,6 +810,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
     {
         FBArgs a = base_args(den, log_emis, lengths, B, N_max);
         a.lat = den_alpha; a.logZ = zd; a.status = seq_status; a.lat_int = 1;
+        a.scale = den_scale;
         if ((r = launch_fb(false, a, s)) != FB_OK) return r;
     }
     cudaStreamWaitEvent(sr->s, sr->fork, 0);
@@ -832,6 +838,7 @@ extern "C" fb_status lfmmi_loss_grad(fb_graph num, fb_graph den, const float *lo
         FBArgs c = base_args(den, log_emis, lengths, B, N_max);
         c.status = seq_status; c.alpha = den_alpha; c.lat_int = 1;
         c.post = grad; c.post_kind = POST_GRAD;
+        if (!std::getenv("FBX_NO_IZ")) { c.ascale_in = den_scale; c.logZ_fwd = zd; }
         if ((r = launch_fb(true, c, s)) != FB_OK) return r;
     }
     cudaStreamWaitEvent(s, sr->join, 0);
