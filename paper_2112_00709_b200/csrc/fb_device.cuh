@@ -311,6 +311,52 @@ __device__ __forceinline__ void phase_a(uint32_t cur, int nsl, int lane, uint32_
     }
 }
 
+// Phase A of the exp-factorised ⊕ (factored mode, the one-CTA den kernels): the same
+// walk as phase_a<MODE_FACTORED>, with the per-slice bookkeeping cut down.
+//  • the warp's first nsl0 slices hold unsplit rows (g = 1, fb_graph.cpp) and run in a
+//    loop without the xor-combine; the split-row slices follow;
+//  • the arc loop is a do-while over an end address (every slice has L ≥ 2 slots);
+//  • every lane stores: lead = row + 1 for row leaders, 0 otherwise, so the store goes to
+//    part[row] or to the scratch cell part[-1] (a_partm1 = &part[-1]) — no branch.  Only a
+//    leader whose sum leaves [2^-80, 2^120] takes the exact fallback.
+__device__ __forceinline__ void phase_a_fact(uint32_t cur, int nsl0, int nsl, int lane, uint32_t a_u, uint32_t a_p,
+                                             uint32_t a_partm1, unsigned long long *ctr) {
+    constexpr float kTiny = 8.271806125530277e-25f;  // 2^-80
+    constexpr float kHuge = 1.329227995784916e+36f;  // 2^120
+    const uint32_t l4 = (uint32_t)lane * 4u, l8 = (uint32_t)lane * 8u;
+    auto slice = [&](auto split) {
+        const uint32_t h = lds_u32(cur + l4);
+        const uint32_t L2 = h >> 19;
+        uint32_t ia = cur + 128u + l4;
+        uint32_t wa = cur + 128u + L2 * 128u + l8;
+        const uint32_t iend = ia + L2 * 128u;
+        float2 a2 = make_float2(0.f, 0.f);
+#pragma unroll 1
+        do {
+            const uint32_t ix = lds_u32(ia);
+            const float2 w2 = lds_f2(wa);
+            const float p0 = lds_v(a_p + (ix & 0xFFFFu), 0.f), p1 = lds_v(a_p + (ix >> 16), 0.f);
+            a2 = __ffma2_rn(make_float2(p0, p1), w2, a2);
+            ia += 128u;
+            wa += 256u;
+        } while (ia != iend);
+        float acc = a2.x + a2.y;
+        int g = 1;
+        if (decltype(split)::value) {
+            g = 1 << ((h >> 16) & 7u);
+            for (int o = 1; o < g; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        }
+        const uint32_t lead = h & 0xFFFFu;
+        float v = lg2(acc);
+        if (!(acc >= kTiny && acc <= kHuge) && lead) v = exact_row(cur, (int)L2, g, lane, a_u, ctr);
+        sts_v(a_partm1 + lead * 4u, v);
+        cur += 128u + L2 * 384u;
+    };
+    int q = 0;
+    for (; q < nsl0; ++q) slice(std::false_type());
+    for (; q < nsl; ++q) slice(std::true_type());
+}
+
 // Write one frame's pdf-level posterior (or gradient) row.  gbuf holds γ in the
 // member's slot order, so pdf slot s sums gbuf[ssp[s] .. ssp[s+1]) (ascending
 // state order, ledger L9); maps staged in shared memory (PdfRegion), addressed
@@ -484,6 +530,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
             }
     }
     const int nsl = S.warp_nsl[gi * W + warp];
+    const int nsl0 = S.warp_nsl0[gi * W + warp];
     const uint32_t mysl = sb + (uint32_t)SL.rec + (uint32_t)S.warp_off[gi * W + warp];
     const bool use_mask = BWD ? G.mask_bwd : G.mask_fwd;
 
@@ -741,7 +788,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         // ---- phase A of frame n_next (+ pdf-level row of the frame finished two frames ago)
         if (IZ) iz_row(n, par);  // gradient row of frame n (its e in gbuf, partials in wz[par])
         else if (pdf_post && pend_n != n) pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pend_n, tid, T, psgn);
-        phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part, G.ctr);
+        if (MODE == MODE_FACTORED) phase_a_fact(mysl, nsl0, nsl, lane, a_u, a_p, a_part - 4, G.ctr);
+        else phase_a<MODE, V>(mysl, nsl, lane, a_u, a_p, a_part, G.ctr);
         __syncthreads();
         // ---- phase B of frame n_next
         const int pp = par;

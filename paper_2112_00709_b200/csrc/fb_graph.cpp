@@ -39,7 +39,7 @@ namespace {
 
 struct HostSched {
     std::vector<unsigned char> blob;           // all members, 16-byte aligned each
-    std::vector<int> rec_bytes, warp_off, warp_nsl;
+    std::vector<int> rec_bytes, warp_off, warp_nsl, warp_nsl0;
     std::vector<long long> rec_off;
     int bytes_max = 0, slots_max = 0;
 };
@@ -110,6 +110,13 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
         heap.push({it.first + sl[q].L + 4, it.second});
     }
     auto slice_bytes = [](const Slice &s) { return (size_t)128 + (size_t)(s.L / 2) * 384; };
+    // inside a warp, the slices of unsplit rows (g = 1) run first: phase A walks them in a
+    // loop without the xor-combine (warp_nsl0 of them), then the split-row slices
+    std::vector<int> warp_nsl0(W, 0);
+    for (int w = 0; w < W; ++w) {
+        std::stable_partition(wsl[w].begin(), wsl[w].end(), [&](int q) { return sl[q].lg == 0; });
+        for (int q : wsl[w]) warp_nsl0[w] += sl[q].lg == 0;
+    }
     std::vector<int> warp_off(W), warp_nsl(W);
     size_t bytes = 0;
     int slots_max = 0;
@@ -305,6 +312,7 @@ bool build_member_sched(const RowLists &rl, int K, int T, int mode, int esize, i
     hs.rec_bytes.push_back((int)bytes);
     hs.warp_off.insert(hs.warp_off.end(), warp_off.begin(), warp_off.end());
     hs.warp_nsl.insert(hs.warp_nsl.end(), warp_nsl.begin(), warp_nsl.end());
+    hs.warp_nsl0.insert(hs.warp_nsl0.end(), warp_nsl0.begin(), warp_nsl0.end());
     hs.bytes_max = std::max<int>(hs.bytes_max, (int)bytes);
     hs.slots_max = std::max(hs.slots_max, slots_max);
     return (long long)K * esize <= 65536;  // byte offsets are 16-bit
@@ -1000,11 +1008,12 @@ static fb_status create_impl(fb_graph *out, int32_t G, const int32_t *state_offs
     size_t o_mo = pk.put(morder);
     std::vector<float> init_nat(log_init, log_init + K_tot), final_nat(log_final, log_final + K_tot);
     size_t o_in = pk.put(init_nat), o_fn = pk.put(final_nat);
-    struct SO { size_t rec, rb, ro, wo, wn; };
+    struct SO { size_t rec, rb, ro, wo, wn, wn0; };
     auto put_sched = [&](HostSched &h) {
         SO o;
         o.rec = pk.put(h.blob); o.rb = pk.put(h.rec_bytes); o.ro = pk.put(h.rec_off); o.wo = pk.put(h.warp_off);
         o.wn = pk.put(h.warp_nsl);
+        o.wn0 = pk.put(h.warp_nsl0);
         return o;
     };
     SO of = put_sched(hf), ob = put_sched(hb), ov = put_sched(hv);
@@ -1067,6 +1076,7 @@ static fb_status create_impl(fb_graph *out, int32_t G, const int32_t *state_offs
     auto set_sched = [&](Sched &d, const SO &o) {
         d.rec = (const unsigned char *)P(o.rec); d.rec_bytes = (const int *)P(o.rb);
         d.rec_off = (const long long *)P(o.ro); d.warp_off = (const int *)P(o.wo); d.warp_nsl = (const int *)P(o.wn);
+        d.warp_nsl0 = (const int *)P(o.wn0);
     };
     set_sched(gr.fwd, of);
     set_sched(gr.bwd, ob);

@@ -42,6 +42,7 @@ struct Sched {
     const long long *rec_off = nullptr; // [G]
     const int *warp_off = nullptr;      // [G*W]
     const int *warp_nsl = nullptr;      // [G*W]
+    const int *warp_nsl0 = nullptr;     // [G*W] how many of them (first) have g = 1 (one-CTA schedules)
     int bytes_max = 0;                  // max rec_bytes
     int slots_max = 0;                  // max arc slots of one warp
 };
@@ -181,7 +182,7 @@ FBX_HD inline SmemLayout smem_layout(int rec_bytes, int K_pad, bool exact, bool 
     L.rec = o; o += fbx_a16((size_t)rec_bytes);
     L.u = o; o += fbx_a16((size_t)K_pad * vsz);
     L.p = o; if (!exact) o += fbx_a16((size_t)K_pad * 4);
-    L.part = o; o += fbx_a16((size_t)K_pad * vsz);
+    L.part = o + 16; o += 16 + fbx_a16((size_t)K_pad * vsz);  // part[-1]: scratch cell of non-leader lanes
     L.gbuf = o; if (gbuf) o += fbx_a16((size_t)K_pad * 4);
     L.red = o; o += fbx_a16(8 * (2 * 32 + 2 * 64) + 64);
     L.total = o;
