@@ -193,7 +193,13 @@ static __device__ __noinline__ float exact_row_c(const int *ptr, const int *src,
 // Combine (m, s) log-sum-exp pairs (m in log2, s ≥ 0) in a fixed order.
 __device__ __forceinline__ void lse2(float &m, float &s, float m2, float s2) { lse_combine<float>(m, s, m2, s2); }
 
-template <bool BWD, int S, int SPT, int T, bool NOP>
+// IZ (backward, −Γ_den gradient of lfmmi_loss_grad): γ normalised through the forward's
+// log Z as in the one-CTA kernel (kModeGradIZ, fb_device.cuh): phase B writes
+// e = 2^{α̂ + β̂ − Ẑ_n} with Ẑ_n = log2 Z − C_n − D_n straight into xbuf, the parts exchange
+// their Σe in the extras slot instead of a (max, sum) pair, and the next frame writes the
+// pdf rows −Σ e / S before its phase A — no posterior pass and, for no-p plans, no extra
+// barrier between the pdf rows and phase B's xbuf writes.
+template <bool BWD, int S, int SPT, int T, bool NOP, bool IZ>
 __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int W = T / 32;
@@ -368,6 +374,25 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     // x = α̂·log2e + β̂ of the frame whose posterior is pending: xbuf[j][s] (shared memory)
     double scale[S];   // C_n / D_n (log2) — identical in every CTA of the cluster
     float vsum[S];
+    // IZ: log2 Z of each sequence's forward; the forward's C of the frame being produced is
+    // staged by lanes s < S of warp 0 (loaded one frame ahead) into cnbuf[s]
+    float zhat[S];
+    double logZ2[S];
+    double cn_reg = 0.0;
+    const uint32_t a_cn = a_red + (uint32_t)((W + 2) * S * kCX) * 4 - 8u * S;  // last S doubles of red
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        zhat[s] = 0.f;
+        logZ2[s] = (IZ && 0 < Ns[s]) ? a.logZ_fwd[bs[s]] * 1.4426950408889634 : 0.0;
+    }
+    auto cn_load = [&](int t) {  // lanes s < S of warp 0: the forward's C_n (natural) of step t
+        if (IZ && tid < S) {
+            int Nss = Ns[0], bss = bs[0];
+#pragma unroll
+            for (int q = 1; q < S; ++q) { Nss = tid == q ? Ns[q] : Nss; bss = tid == q ? bs[q] : bss; }
+            cn_reg = (t < Nss) ? __ldg(a.ascale_in + (size_t)bss * N_max + (Nss - 1 - t)) : 0.0;
+        }
+    };
 #pragma unroll
     for (int s = 0; s < S; ++s) { scale[s] = 0.0; vsum[s] = 0.f; }
     // termination pairs are reduced per warp at each sequence's last frame: red fields 3, 4
@@ -401,7 +426,17 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             for (int k = 1; k < SPT; ++k) mx = fmaxf(mx, u[k][s]);
             mx = warp_max_fast(mx);
             if (lane == 0) sts_v(a_red + (uint32_t)((warp * S + s) * kCX) * 4, mx);
-            if (want_post) {
+            if (IZ) {  // e = 2^{x − Ẑ} into xbuf, per-warp Σ e into red field 1
+                float es = 0.f;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) {
+                    const float e = ex2(fmaf(ar[k][s], L2E, h[k][s]) - zhat[s]);  // 0 for non-viable / padding
+                    if (tid + k * T < Kc) sts_v(a_xbuf + (uint32_t)((tid + k * T) * S + s) * 4, e);
+                    es += e;
+                }
+                es = warp_sum(es);
+                if (lane == 0) sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 1) * 4, es);
+            } else if (want_post) {
                 float x[SPT];
 #pragma unroll
                 for (int k = 0; k < SPT; ++k) {
@@ -465,7 +500,9 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 const uint32_t r = a_red + (uint32_t)((lane * S + s) * kCX) * 4;
                 const float mx = warp_max_fast(lane < W ? lds_v(r, 0.f) : NEG_INF);
                 float zm = NEG_INF, zs = 0.f;
-                if (want_post) {
+                if (IZ) {
+                    zm = warp_sum(lane < W ? lds_v(r + 4, 0.f) : 0.f);  // the part's Σ e
+                } else if (want_post) {
                     const float pm = lane < W ? lds_v(r + 4, 0.f) : NEG_INF;
                     const float ps = lane < W ? lds_v(r + 8, 0.f) : 0.f;
                     zm = warp_max_fast(pm);
@@ -486,12 +523,15 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             for (int w = lane >> 2; w < W; w += 8) {
                 const uint32_t r = a_red + (uint32_t)((w * S + s) * kCX) * 4;
                 mx = fmaxf(mx, lds_v(r, 0.f));
-                if (want_post) lse2(zm, zs, lds_v(r + 4, 0.f), lds_v(r + 8, 0.f));
+                if (IZ) zs += lds_v(r + 4, 0.f);
+                else if (want_post) lse2(zm, zs, lds_v(r + 4, 0.f), lds_v(r + 8, 0.f));
             }
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                if (want_post) {
+                if (IZ) {
+                    zs += __shfl_xor_sync(0xffffffffu, zs, o);
+                } else if (want_post) {
                     const float m2 = __shfl_xor_sync(0xffffffffu, zm, o), s2 = __shfl_xor_sync(0xffffffffu, zs, o);
                     lse2(zm, zs, m2, s2);
                 }
@@ -499,7 +539,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             if (lane < S) {
                 const uint32_t x = a_x(t, cr, s);
                 sts_v(x, mx);
-                sts_v(x + 4, zm);
+                sts_v(x + 4, IZ ? zs : zm);
                 sts_v(x + 8, zs);
             }
         }
@@ -568,6 +608,9 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             for (int k = 0; k < SPT; ++k) { h[k][s] -= c; u[k][s] -= c; }
             if (cr == 0 && tid == 0 && a.scale && 0 < Ns[s])
                 a.scale[(size_t)bs[s] * N_max + frame(s, 0)] = scale[s] * kLN2;
+            if (IZ && 0 < Ns[s])
+                zhat[s] = (float)(logZ2[s] - __ldg(a.ascale_in + (size_t)bs[s] * N_max + frame(s, 0)) * 1.4426950408889634 -
+                                  scale[s]);
         }
         emit(0, h, u);
         fence_async_smem();
@@ -584,8 +627,44 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     const int nsl_loc = split ? SC.warp_nsl[2 * cr * W + warp] : 0;
     const uint32_t mysl_loc = a_rec + (uint32_t)(split ? SC.warp_off[2 * cr * W + warp] : 0);
     const int own0 = k0 * S, own1 = (k0 + Kc) * S;  // this part's element range of u / p
+    cn_load(1);
+    // pdf-level rows of frame t−1 for this part's pdf range (ascending states, ledger L9); IZ: the
+    // e of xbuf scaled by mul[s] = −1/S_{t−1}, else γ of gbuf with the sign of the output kind
+    auto pdf_rows = [&](int t, const float (&mul)[S]) {
+        const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;
+        const uint32_t src = IZ ? a_xbuf : a_gbuf;
+        // one thread per (pdf, sequence) pair (a part owns few pdfs: N2 ~21 × ~36 states),
+        // two interleaved accumulators; consecutive threads write consecutive pdfs
+        const int nd = d_hi - d_lo;
+        for (int pr = tid; pr < nd * S; pr += T) {
+            const int s = pr / nd, d = d_lo + pr % nd;
+            int Nss = Ns[0];
+            float ms = mul[0];
+#pragma unroll
+            for (int q = 1; q < S; ++q) { Nss = s == q ? Ns[q] : Nss; ms = s == q ? mul[q] : ms; }
+            if (t - 1 >= Nss) continue;
+            int bss = bs[0];
+#pragma unroll
+            for (int q = 1; q < S; ++q) bss = s == q ? bs[q] : bss;
+            const uint32_t w = lds_u32(a_pq + 4u * (uint32_t)(d - d_lo));
+            const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
+            float acc0 = 0.f, acc1 = 0.f;
+            uint32_t ga = src + (uint32_t)(q0 * S + s) * 4;
+            uint32_t i = 0;
+            for (; i + 1 < c; i += 2, ga += 8u * S) {
+                acc0 += lds_v(ga, 0.f);
+                acc1 += lds_v(ga + 4u * S, 0.f);
+            }
+            if (i < c) acc0 += lds_v(ga, 0.f);
+            a.post[((size_t)bss * N_max + (BWD ? Nss - 1 - (t - 1) : t - 1)) * D + d] = (IZ ? ms : sgn) * (acc0 + acc1);
+        }
+    };
     for (int t = 1; t <= Tmax; ++t) {
         const bool last = t == Tmax;
+        if (IZ && tid < S) {  // the forward's C of step t (loaded last frame) → cnbuf; load step t + 1's
+            asm volatile("st.shared.f64 [%0], %1;" ::"r"(a_cn + 8u * (uint32_t)tid), "d"(cn_reg));
+            cn_load(t + 1);
+        }
         if (!last) {
             if (want_post) load_alpha(t);
             emis_issue(t + 1);
@@ -612,28 +691,34 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         // then lane s broadcasts sequence s
         float cmax[S], Z[S];
         {
-            float mx = NEG_INF, zm = NEG_INF, zs = 0.f;
+            float mx = NEG_INF, zm = IZ ? 0.f : NEG_INF, zs = 0.f;
             if (lane < C * S) {
                 const uint32_t x = a_x(t - 1, lane / S, lane % S);
                 mx = lds_v(x, 0.f);
-                if (want_post) { zm = lds_v(x + 4, 0.f); zs = lds_v(x + 8, 0.f); }
+                if (IZ) zm = lds_v(x + 4, 0.f);
+                else if (want_post) { zm = lds_v(x + 4, 0.f); zs = lds_v(x + 8, 0.f); }
             }
             for (int o = S; o < C * S; o <<= 1) {
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                if (want_post) {
+                if (IZ) {
+                    zm += __shfl_xor_sync(0xffffffffu, zm, o);  // Σ e over the parts (commutative tree)
+                } else if (want_post) {
                     const float m2 = __shfl_xor_sync(0xffffffffu, zm, o), s2 = __shfl_xor_sync(0xffffffffu, zs, o);
                     lse2(zm, zs, m2, s2);
                 }
             }
-            const float zl = (zm == NEG_INF) ? NEG_INF : zm + lg2(zs);
+            // IZ: Z[s] carries the pdf-row multiplier −1/S (0 if S is not a positive finite sum)
+            const float zl = IZ ? ((zm > 0.f && zm < INFINITY) ? -1.f / zm : 0.f)
+                                : ((zm == NEG_INF) ? NEG_INF : zm + lg2(zs));
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 cmax[s] = __shfl_sync(0xffffffffu, mx, s);
                 Z[s] = want_post ? __shfl_sync(0xffffffffu, zl, s) : NEG_INF;
             }
         }
+        if (IZ) pdf_rows(t, Z);  // frame t−1's e (xbuf) is complete; phase B refills xbuf after the barrier
         // posteriors of frame t−1 (Eq. (15), normalised by Z_{t−1} = LSE_k(α̂ + β̂))
-        if (want_post) {
+        if (want_post && !IZ) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 if (t - 1 >= Ns[s]) continue;
@@ -662,33 +747,8 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         if (!last) phase_a_vec<S, false>(mysl, nsl, lane, NOP ? up : a_p, a_part, split);
         cpa_wait1();
         __syncthreads();  // part rows, γ rows, step-t emissions complete
-        // pdf-level rows of frame t−1 for this part's pdf range (ascending states, ledger L9)
-        if (pdf_post) {
-            const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;
-            // one thread per (pdf, sequence) pair (a part owns few pdfs: N2 ~21 × ~36 states),
-            // two interleaved accumulators; consecutive threads write consecutive pdfs
-            const int nd = d_hi - d_lo;
-            for (int pr = tid; pr < nd * S; pr += T) {
-                const int s = pr / nd, d = d_lo + pr % nd;
-                int Nss = Ns[0];
-#pragma unroll
-                for (int q = 1; q < S; ++q) Nss = s == q ? Ns[q] : Nss;
-                if (t - 1 >= Nss) continue;
-                int bss = bs[0];
-#pragma unroll
-                for (int q = 1; q < S; ++q) bss = s == q ? bs[q] : bss;
-                const uint32_t w = lds_u32(a_pq + 4u * (uint32_t)(d - d_lo));
-                const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
-                float acc0 = 0.f, acc1 = 0.f;
-                uint32_t ga = a_gbuf + (uint32_t)(q0 * S + s) * 4;
-                uint32_t i = 0;
-                for (; i + 1 < c; i += 2, ga += 8u * S) {
-                    acc0 += lds_v(ga, 0.f);
-                    acc1 += lds_v(ga + 4u * S, 0.f);
-                }
-                if (i < c) acc0 += lds_v(ga, 0.f);
-                a.post[((size_t)bss * N_max + (BWD ? Nss - 1 - (t - 1) : t - 1)) * D + d] = sgn * (acc0 + acc1);
-            }
+        if (pdf_post && !IZ) {
+            pdf_rows(t, Z);
             if (NOP) __syncthreads();  // γ lives in xbuf, which phase B refills with the next x
         }
         if (last) break;
@@ -704,6 +764,11 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             if (act) {
                 scale[s] += (double)c[s];
                 if (cr == 0 && tid == 0 && a.scale) a.scale[(size_t)bs[s] * N_max + frame(s, t)] = scale[s] * kLN2;
+                if (IZ) {
+                    double cn;
+                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cn) : "r"(a_cn + 8u * (uint32_t)s));
+                    zhat[s] = (float)(logZ2[s] - cn * 1.4426950408889634 - scale[s]);
+                }
             }
         }
 #pragma unroll
@@ -809,32 +874,41 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 using KFn = void (*)(FBArgs);
 // T = 1024 threads (SPT ≤ 4, ≤ 64 registers) or 512 (SPT ≤ 8, ≤ 128 registers);
 // nop (S = 4 only): no p array
-template <bool BWD, int S, bool NOP>
+template <bool BWD, int S, bool NOP, bool IZ>
 static KFn pick_fbc_t(int spt, int T) {
     if (T == 1024) {
         switch (spt) {
-            case 1: return k_fbc<BWD, S, 1, 1024, NOP>;
-            case 2: return k_fbc<BWD, S, 2, 1024, NOP>;
-            case 3: return k_fbc<BWD, S, 3, 1024, NOP>;
-            default: return k_fbc<BWD, S, 4, 1024, NOP>;
+            case 1: return k_fbc<BWD, S, 1, 1024, NOP, IZ>;
+            case 2: return k_fbc<BWD, S, 2, 1024, NOP, IZ>;
+            case 3: return k_fbc<BWD, S, 3, 1024, NOP, IZ>;
+            default: return k_fbc<BWD, S, 4, 1024, NOP, IZ>;
         }
     }
     switch (spt) {
-        case 1: return k_fbc<BWD, S, 1, 512, NOP>;
-        case 2: return k_fbc<BWD, S, 2, 512, NOP>;
-        case 3: return k_fbc<BWD, S, 3, 512, NOP>;
-        case 4: return k_fbc<BWD, S, 4, 512, NOP>;
-        case 6: return k_fbc<BWD, S, 6, 512, NOP>;
-        default: return k_fbc<BWD, S, 8, 512, NOP>;
+        case 1: return k_fbc<BWD, S, 1, 512, NOP, IZ>;
+        case 2: return k_fbc<BWD, S, 2, 512, NOP, IZ>;
+        case 3: return k_fbc<BWD, S, 3, 512, NOP, IZ>;
+        case 4: return k_fbc<BWD, S, 4, 512, NOP, IZ>;
+        case 6: return k_fbc<BWD, S, 6, 512, NOP, IZ>;
+        default: return k_fbc<BWD, S, 8, 512, NOP, IZ>;
     }
 }
+// iz (backward only): the lfmmi −Γ_den epilogue normalised through the forward's log Z
 template <bool BWD, int S>
-KFn pick_fbc(int spt, int T, int nop) {
-    if constexpr (S == 4) {
-        if (nop) return pick_fbc_t<BWD, S, true>(spt, T);
+KFn pick_fbc(int spt, int T, int nop, int iz) {
+    if constexpr (BWD) {
+        if (iz) {
+            if constexpr (S == 4) {
+                if (nop) return pick_fbc_t<BWD, S, true, true>(spt, T);
+            }
+            return pick_fbc_t<BWD, S, false, true>(spt, T);
+        }
     }
-    return pick_fbc_t<BWD, S, false>(spt, T);
+    if constexpr (S == 4) {
+        if (nop) return pick_fbc_t<BWD, S, true, false>(spt, T);
+    }
+    return pick_fbc_t<BWD, S, false, false>(spt, T);
 }
-template KFn pick_fbc<(bool)FBX_BWD, FBX_S>(int, int, int);
+template KFn pick_fbc<(bool)FBX_BWD, FBX_S>(int, int, int, int);
 
 }  // namespace fbx

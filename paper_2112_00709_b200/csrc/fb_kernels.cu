@@ -492,11 +492,11 @@ static fb_status check_launch(const char *what) {
 }
 
 template <bool BWD, int S>
-KFn pick_fbc(int spt, int T, int nop);
-extern template KFn pick_fbc<false, 2>(int, int, int);
-extern template KFn pick_fbc<false, 4>(int, int, int);
-extern template KFn pick_fbc<true, 2>(int, int, int);
-extern template KFn pick_fbc<true, 4>(int, int, int);
+KFn pick_fbc(int spt, int T, int nop, int iz);
+extern template KFn pick_fbc<false, 2>(int, int, int, int);
+extern template KFn pick_fbc<false, 4>(int, int, int, int);
+extern template KFn pick_fbc<true, 2>(int, int, int, int);
+extern template KFn pick_fbc<true, 4>(int, int, int, int);
 
 // Does this launch run the cluster-batched kernel k_fbc (fb_cluster.cu)?
 static bool use_cluster(bool bwd, const FBArgs &a, bool raw) {
@@ -516,8 +516,10 @@ static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
     const CPlan &P = G.cp;
     FBArgs aa = a;
     aa.tma = (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0);  // 16-byte emission copies
-    KFn fn = bwd ? (P.S == 4 ? pick_fbc<true, 4>(P.spt, P.T, P.nop) : pick_fbc<true, 2>(P.spt, P.T, 0))
-                 : (P.S == 4 ? pick_fbc<false, 4>(P.spt, P.T, P.nop) : pick_fbc<false, 2>(P.spt, P.T, 0));
+    // the lfmmi den backward normalises γ through the forward's log Z (IZ, fb_cluster.cu)
+    const int iz = bwd && a.post_kind == POST_GRAD && a.ascale_in && a.logZ_fwd;
+    KFn fn = bwd ? (P.S == 4 ? pick_fbc<true, 4>(P.spt, P.T, P.nop, iz) : pick_fbc<true, 2>(P.spt, P.T, 0, iz))
+                 : (P.S == 4 ? pick_fbc<false, 4>(P.spt, P.T, P.nop, 0) : pick_fbc<false, 2>(P.spt, P.T, 0, 0));
     const size_t sm = cl_layout(bwd ? P.bwd.bytes_max : P.fwd.bytes_max, P.K_int, P.Kc_max, P.Dc_max, P.S, P.C,
                                 P.T / 32, bwd, P.nop != 0).total;
     if (fb_status r0 = set_smem((const void *)fn, sm); r0 != FB_OK) return r0;
