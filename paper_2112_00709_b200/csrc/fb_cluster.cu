@@ -127,9 +127,10 @@ __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uin
         const int row = (int)(h & 0xFFFFu) - 1, lg = (int)((h >> 16) & 7u), L2 = (int)(h >> 19);
         uint32_t ia = cur + 128 + lane * 4;
         uint32_t wa = cur + 128 + (uint32_t)L2 * 128 + lane * 8;
-        float a0[S], a1[S];
+        // sequence pairs accumulate with packed FFMA2 (sm_100 f32x2): one per arc and pair
+        float2 a0[S / 2], a1[S / 2];
 #pragma unroll
-        for (int i = 0; i < S; ++i) { a0[i] = 0.f; a1[i] = 0.f; }
+        for (int i = 0; i < S / 2; ++i) { a0[i] = make_float2(0.f, 0.f); a1[i] = make_float2(0.f, 0.f); }
 #pragma unroll 2
         for (int s = 0; s < L2; ++s) {
             const uint32_t ix = lds_u32(ia);
@@ -142,16 +143,16 @@ __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uin
                 for (int i = 0; i < S; ++i) { p0[i] = ex2(p0[i]); p1[i] = ex2(p1[i]); }
             }
 #pragma unroll
-            for (int i = 0; i < S; ++i) {
-                a0[i] = fmaf(p0[i], w2.x, a0[i]);
-                a1[i] = fmaf(p1[i], w2.y, a1[i]);
+            for (int i = 0; i < S / 2; ++i) {
+                a0[i] = __ffma2_rn(make_float2(p0[2 * i], p0[2 * i + 1]), make_float2(w2.x, w2.x), a0[i]);
+                a1[i] = __ffma2_rn(make_float2(p1[2 * i], p1[2 * i + 1]), make_float2(w2.y, w2.y), a1[i]);
             }
             ia += 128;
             wa += 256;
         }
         float acc[S];
 #pragma unroll
-        for (int i = 0; i < S; ++i) acc[i] = a0[i] + a1[i];
+        for (int i = 0; i < S / 2; ++i) { acc[2 * i] = a0[i].x + a1[i].x; acc[2 * i + 1] = a0[i].y + a1[i].y; }
         for (int o = 1; o < (1 << lg); o <<= 1) {
 #pragma unroll
             for (int i = 0; i < S; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             const uint32_t base = a_ebuf + (uint32_t)(t & 1) * EB;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                if (t >= Ns[s]) continue;
+                if (t >= Ns[s] || (e16 ? 4 * tid : tid) >= e_len) continue;  // only the copying threads
                 const float *src = a.emis + ((size_t)bs[s] * N_max + frame(s, t)) * D + e_lo;
                 const uint32_t dst = base + (uint32_t)s * DC4;
                 if (e16) {
@@ -671,7 +672,10 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             // split: this part's own-source arcs while the other parts' rows are in flight
             if (split) phase_a_vec<S, false>(mysl_loc, nsl_loc, lane, NOP ? a_u(t - 1) : a_p, a_part, true);
         }
-        mbar_wait_sleep(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
+        // no-p plans: warp 0 alone polls the exchange barrier (acquire); the CTA barrier below
+        // orders the other warps' reads of the received rows after it (with-p plans convert
+        // the received rows before that barrier, so every warp waits)
+        if (!NOP || warp == 0) mbar_wait_sleep(a_mbar + 8u * (uint32_t)((t - 1) & 1), (uint32_t)(((t - 1) >> 1) & 1));
         const uint32_t up = a_u(t - 1);
         if (!last && !NOP) {  // p = 2^u of the other parts' rows
             for (int e = 4 * tid; e < Kint * S; e += 4 * T) {
