@@ -47,15 +47,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     cmds, objs = [], []
+    hdr_t = max(os.path.getmtime(os.path.join(CSRC, h)) for h in HEADERS)
     for src, obj, extra in _units():
         obj = os.path.join(CSRC, OBJ_TAG + obj)
+        objs.append(obj)
+        # an object newer than its source, the headers and this script (flags) is up to date
+        if not force and not EXTRA and os.path.exists(obj) and os.path.getmtime(obj) > max(
+                hdr_t, os.path.getmtime(os.path.join(CSRC, src)), os.path.getmtime(__file__)):
+            continue
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
                *extra, *EXTRA, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu") and verbose:
             cmd[1:1] = ["-Xptxas", "-v"]
         cmds.append(cmd)
-        objs.append(obj)
-    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
         for f in [ex.submit(subprocess.check_call, c) for c in cmds]:
             f.result()
     tmp = LIB + f".tmp{os.getpid()}"
