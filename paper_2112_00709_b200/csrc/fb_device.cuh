@@ -716,7 +716,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     auto iz_row = [&](int pn, int pp) {
         float sv = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + lane) * 8, 0.f) : 0.f;
         sv = warp_sum(sv);  // every warp the same S (same partials, same order)
-        const float mul = (sv > 0.f && sv < INFINITY) ? -1.f / sv : 0.f;
+        const float mul = (sv > 0.f && sv < INFINITY) ? -__fdividef(1.f, sv) : 0.f;
         pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pn, tid, T, mul);
     };
     auto block_max_prev = [&](int pp) {
@@ -805,21 +805,28 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         V h[SPT];
         float vv[SPT];
         fetch_v(tstep, vb, vv);
+        // graphs without masked states: every real state is viable and an inert slot's part
+        // row is 0̄ (never written), so the test is skipped (a non-finite emission read by an
+        // inert slot only reaches outputs of a sequence that vsum flags anyway)
+        auto states = [&](auto masked) {
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-            const V y = lds_v(a_part + (uint32_t)(tid + k * T) * VS, (V)0);
-            const bool ok = viable(k, n);
-            const float v = vv[k];
-            vsum += v;
-            const V v2 = (V)v * L2E;
-            if (!BWD) {
-                h[k] = ok ? y + v2 - c : NINF;
-                uk[k] = h[k];
-            } else {
-                h[k] = ok ? y - c : NINF;
-                uk[k] = h[k] + v2;
+            for (int k = 0; k < SPT; ++k) {
+                const V y = lds_v(a_part + (uint32_t)(tid + k * T) * VS, (V)0);
+                const bool ok = decltype(masked)::value ? viable(k, n) : true;
+                const float v = vv[k];
+                vsum += v;
+                const V v2 = (V)v * L2E;
+                if (!BWD) {
+                    h[k] = ok ? y + v2 - c : NINF;
+                    uk[k] = h[k];
+                } else {
+                    h[k] = ok ? y - c : NINF;
+                    uk[k] = h[k] + v2;
+                }
             }
-        }
+        };
+        if (use_mask) states(std::true_type());
+        else states(std::false_type());
         emit(n, h, ab);
         load_v(n + 2 * dir, vb);  // refill with the frame two steps ahead
         if (want_post) load_alpha(n + 2 * dir, ab);
