@@ -83,6 +83,10 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
+            t0 = time.time()  # nvidia-smi is up (first row) before the timed region starts
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.01)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -249,6 +253,7 @@ def ncu_traffic(args, n_launch: int):
             d["bytes"] += v * scale
     out = {}
     for (_, kname), d in sorted(per.items(), key=lambda x: int(x[0][0])):
+        kname = kname.split(" ", 1)[1] if kname.startswith("void ") else kname  # ncu prints "void k_fbc<…>(FBArgs)"
         label = ("k_fbc" if kname.startswith("k_fbc") else "k_fb") + ("_bwd[G=1]" if "<true" in kname or "<1" in kname
                                                                       else "_fwd[G=1]")
         out.setdefault(label, d["bytes"])

@@ -7,7 +7,7 @@ cd "$(dirname "$0")/.."
 T=${TAG:-r2}
 O=gpurun_out
 python bench.py > $O/${T}_bench_c4.json 2> $O/${T}_bench_c4.err; echo "c4 rc=$?"
-for w in c3 paper c5-weak c5-strong viterbi viterbi-paper; do
+for w in c2 c3 paper c5-weak c5-strong viterbi viterbi-paper; do
   python bench.py --workload $w --no-cpu-baseline > $O/${T}_bench_$w.json 2> $O/${T}_bench_$w.err; echo "$w rc=$?"
 done
 python bench.py --impl reference > $O/${T}_bench_reference.json 2> $O/${T}_bench_reference.err; echo "ref rc=$?"
@@ -21,6 +21,7 @@ for w in c4 paper; do
   for i in 0 1 2; do python tools/ncu_lines.py /tmp/${T}_$w.ncu-rep $i 40 > $O/${T}_ncu_${w}_lines$i.txt 2>&1; done
   ncu -i /tmp/${T}_$w.ncu-rep --page raw --csv > $O/${T}_ncu_${w}_raw.csv 2>/dev/null
 done
+python -m tests.parity_report > $O/${T}_parity_errors.txt 2>&1; echo "parity rc=$?"
 for t in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $t --log-file $O/${T}_sanitizer_$t.log python tools/sanitize.py > $O/san_$t.out 2>&1
   echo "$t rc=$? $(tail -1 $O/${T}_sanitizer_$t.log)"
