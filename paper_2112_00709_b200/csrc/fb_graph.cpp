@@ -982,7 +982,7 @@ static fb_status create_impl(fb_graph *out, int32_t G, const int32_t *state_offs
             if (cs.C < 2 || cs.C > 8 || !(cs.S == 2 || cs.S == 4) || (cs.nop && cs.S != 4)) continue;
             const char *le = std::getenv("FBX_CLUSTER_LMAX");
             if (build_cluster_plan(in0, out0, K_tot, D, pdf, dist_fin, dist_start, init2, final2, cs.C, cs.S,
-                                   le ? std::max(1, std::atoi(le)) : 24, hcp,  // 24: N2 bwd 5.88 -> 5.73 ms vs 12
+                                   le ? std::max(1, std::atoi(le)) : 32, hcp,  // N2 step: 12 -> 24 -> 32: 9.70 -> 9.55 -> 8.95 ms (48: 9.23)
                                    0, cs.nop != 0)) { cp_ok = true; break; }
         }
     }
