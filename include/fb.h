@@ -216,7 +216,8 @@ fb_status fb_gap(fb_graph g, const float *alpha, const double *alpha_scale, cons
 
 /*
  * fb_workspace_bytes — device workspace lfmmi_loss_grad needs for (num, den, B, N_max):
- * the α̂ lattices of both graphs, their scales and the numerator pdf posteriors.
+ * the α̂ lattices of both graphs, the denominator forward's per-frame offsets C_n,
+ * both log Z vectors and the numerator pdf posteriors.
  */
 size_t fb_workspace_bytes(fb_graph num, fb_graph den, int32_t B, int32_t N_max);
 
@@ -225,7 +226,11 @@ size_t fb_workspace_bytes(fb_graph num, fb_graph den, int32_t B, int32_t N_max);
  *   loss[b] = log p(X_b | G_num,b) − log p(X_b | G_den) = logZ_num − logZ_den
  *   grad[b,n,d] = ∂ℒ/∂φ_{n,d} = Γ_num,n(d) − Γ_den,n(d)
  * for n < N_b, 0 for padded frames (ledger L17).  ℒ is per utterance,
- * unnormalised, the ascent direction as printed (ledger L10).
+ * unnormalised, the ascent direction as printed (ledger L10).  Γ_den of frame n
+ * is normalised through the forward's log Z (Eq. (1); ledger L22):
+ * e_k = exp(α̂_n(k) + β̂_n(k) − (log Z − C_n − D_n)), Γ_den,n(d) = Σ_{pdf(k)=d} e_k / Σ_k e_k.
+ * The numerator and denominator passes run concurrently (the numerator on the
+ * SMs the denominator leaves idle); the call is ordered on `stream` as a whole.
  *
  *   num         G == B graph handle (one numerator graph per sequence).
  *   den         G == 1 graph handle (shared denominator graph); num->D == den->D.
