@@ -634,30 +634,36 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     auto pdf_rows = [&](int t, const float (&mul)[S]) {
         const float sgn = a.post_kind == POST_GRAD ? -1.f : 1.f;
         const uint32_t src = IZ ? a_xbuf : a_gbuf;
-        // one thread per (pdf, sequence) pair (a part owns few pdfs: N2 ~21 × ~36 states),
-        // two interleaved accumulators; consecutive threads write consecutive pdfs
-        const int nd = d_hi - d_lo;
-        for (int pr = tid; pr < nd * S; pr += T) {
-            const int s = pr / nd, d = d_lo + pr % nd;
-            int Nss = Ns[0];
+        // four lanes per (pdf, sequence) pair (a part owns few pdfs with many states: N2 ~21 pdfs ×
+        // ~36 states): lane i of the quad sums states i, i + 4, …, two xor shuffles combine the quad,
+        // so the rows cost every warp a few gathers instead of ~36 serial ones on three warps
+        constexpr int PL = 4;
+        const int nd = d_hi - d_lo, npairs = nd * S;
+        for (int base = 0; base < npairs * PL; base += T) {  // CTA-uniform trip count (full-warp shuffles)
+            const int idx = base + tid, pr = idx / PL, sub = idx & (PL - 1);
+            const bool on = pr < npairs;
+            int s = 0, d = d_lo;
+            float acc = 0.f;
+            if (on) {
+                s = pr / nd;
+                d = d_lo + pr % nd;
+                const uint32_t w = lds_u32(a_pq + 4u * (uint32_t)(d - d_lo));
+                const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
+                for (uint32_t i = (uint32_t)sub; i < c; i += PL) acc += lds_v(src + ((q0 + i) * S + (uint32_t)s) * 4u, 0.f);
+            }
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            if (!on || sub != 0) continue;
+            int Nss = Ns[0], bss = bs[0];
             float ms = mul[0];
 #pragma unroll
-            for (int q = 1; q < S; ++q) { Nss = s == q ? Ns[q] : Nss; ms = s == q ? mul[q] : ms; }
-            if (t - 1 >= Nss) continue;
-            int bss = bs[0];
-#pragma unroll
-            for (int q = 1; q < S; ++q) bss = s == q ? bs[q] : bss;
-            const uint32_t w = lds_u32(a_pq + 4u * (uint32_t)(d - d_lo));
-            const uint32_t q0 = w & 0xFFFFu, c = w >> 16;
-            float acc0 = 0.f, acc1 = 0.f;
-            uint32_t ga = src + (uint32_t)(q0 * S + s) * 4;
-            uint32_t i = 0;
-            for (; i + 1 < c; i += 2, ga += 8u * S) {
-                acc0 += lds_v(ga, 0.f);
-                acc1 += lds_v(ga + 4u * S, 0.f);
+            for (int q = 1; q < S; ++q) {
+                Nss = s == q ? Ns[q] : Nss;
+                bss = s == q ? bs[q] : bss;
+                ms = s == q ? mul[q] : ms;
             }
-            if (i < c) acc0 += lds_v(ga, 0.f);
-            a.post[((size_t)bss * N_max + (BWD ? Nss - 1 - (t - 1) : t - 1)) * D + d] = (IZ ? ms : sgn) * (acc0 + acc1);
+            if (t - 1 >= Nss) continue;
+            a.post[((size_t)bss * N_max + (BWD ? Nss - 1 - (t - 1) : t - 1)) * D + d] = (IZ ? ms : sgn) * acc;
         }
     };
     for (int t = 1; t <= Tmax; ++t) {
