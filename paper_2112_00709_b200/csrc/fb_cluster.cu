@@ -766,12 +766,19 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         const uint32_t eb = a_ebuf + (uint32_t)(t & 1) * EB;
         float c[S];
         int lim[S];
+        // the float64 offsets are needed by every thread only for IZ (Ẑ); otherwise warp 0 of
+        // part 0 keeps them (termination, the scale output) — a CTA-uniform branch
+        const bool keep_scale = IZ || (cr == 0 && warp == 0);
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const bool act = t < Ns[s];
             c[s] = (cmax[s] == NEG_INF) ? 0.f : cmax[s];  // no viable state: keep 0̄ everywhere
             lim[s] = act ? (BWD ? frame(s, t) : Ns[s] - 1 - t) : -1;
-            if (act) {
+        }
+        if (keep_scale) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                if (t >= Ns[s]) continue;
                 scale[s] += (double)c[s];
                 if (cr == 0 && tid == 0 && a.scale) a.scale[(size_t)bs[s] * N_max + frame(s, t)] = scale[s] * kLN2;
                 if (IZ) {
@@ -790,13 +797,15 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 const float z[S] = {};
                 VS<S>::st(a_part + (uint32_t)(j * S) * 4, z);
             }
-            bool bad = false;
+            float alo = 1.f, ahi = 1.f;  // range of the viable sums (the fallback test, once per state)
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const float v = lds_v(eb + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
                 vsum[s] += lim[s] >= 0 ? v : 0.f;  // inactive sequences' buffers are stale
                 const bool ok = distk[k] <= lim[s];
-                bad |= ok && !(acc[s] >= kTiny && acc[s] <= kHuge);
+                const float am = ok ? acc[s] : 1.f;
+                alo = fminf(alo, am);
+                ahi = fmaxf(ahi, am);
                 const float y = lg2(acc[s]);
                 if (!BWD) {
                     h[k][s] = ok ? y + fmaf(v, L2E, -c[s]) : NEG_INF;
@@ -806,7 +815,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                     u[k][s] = ok ? fmaf(v, L2E, h[k][s]) : NEG_INF;
                 }
             }
-            if (bad) {  // exact max-then-sum rows (rare)
+            if (!(alo >= kTiny && ahi <= kHuge)) {  // exact max-then-sum rows (rare)
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
                     if (!(distk[k] <= lim[s]) || (acc[s] >= kTiny && acc[s] <= kHuge)) continue;
