@@ -191,6 +191,34 @@ static __device__ __noinline__ float exact_row_c(const int *ptr, const int *src,
     return m == NEG_INF ? NEG_INF : m + log2f(sum);
 }
 
+// Warp sums of S values per lane (S = 2^m) by reduce-scatter: at offsets 16, 8, …
+// each lane keeps half of its values and adds its partner's copy of them, then a plain
+// butterfly finishes; lane l ends with the sum of the sequence `seq` it returns
+// (determined by its bits 4 … 5−m); lanes with those bits only (l % (32 >> m) == 0)
+// hold distinct sequences.  log2(S) + 5 − log2(S) = 5 shuffles for all S sums.
+template <int S>
+__device__ __forceinline__ float warp_sum_scatter(const float (&v)[S], int lane, int &seq) {
+    float cur[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) cur[i] = v[i];
+    int base = 0, off = 16;
+#pragma unroll
+    for (int nn = S; nn > 1; nn >>= 1, off >>= 1) {
+        const bool up = (lane & off) != 0;
+#pragma unroll
+        for (int i = 0; i < nn / 2; ++i) {
+            const float keep = up ? cur[i + nn / 2] : cur[i];
+            const float send = up ? cur[i] : cur[i + nn / 2];
+            cur[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+        base += up ? nn / 2 : 0;
+    }
+    float r = cur[0];
+    for (; off; off >>= 1) r += __shfl_xor_sync(0xffffffffu, r, off);
+    seq = base;
+    return r;
+}
+
 // Combine (m, s) log-sum-exp pairs (m in log2, s ≥ 0) in a fixed order.
 __device__ __forceinline__ void lse2(float &m, float &s, float m2, float s2) { lse_combine<float>(m, s, m2, s2); }
 
@@ -427,16 +455,8 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             for (int k = 1; k < SPT; ++k) mx = fmaxf(mx, u[k][s]);
             mx = warp_max_fast(mx);
             if (lane == 0) sts_v(a_red + (uint32_t)((warp * S + s) * kCX) * 4, mx);
-            if (IZ) {  // e = 2^{x − Ẑ} into xbuf, per-warp Σ e into red field 1
-                float es = 0.f;
-#pragma unroll
-                for (int k = 0; k < SPT; ++k) {
-                    const float e = ex2(fmaf(ar[k][s], L2E, h[k][s]) - zhat[s]);  // 0 for non-viable / padding
-                    if (tid + k * T < Kc) sts_v(a_xbuf + (uint32_t)((tid + k * T) * S + s) * 4, e);
-                    es += e;
-                }
-                es = warp_sum(es);
-                if (lane == 0) sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 1) * 4, es);
+            if (IZ) {
+                // below, for all sequences at once
             } else if (want_post) {
                 float x[SPT];
 #pragma unroll
@@ -467,6 +487,24 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                     sts_v(a_red + (uint32_t)((warp * S + s) * kCX + 4) * 4, ts);
                 }
             }
+        }
+        if (IZ) {  // e = 2^{x − Ẑ} into xbuf (one vector store per state), per-warp Σ e into red field 1
+            float es[S];
+#pragma unroll
+            for (int s = 0; s < S; ++s) es[s] = 0.f;
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                float e[S];
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    e[s] = ex2(fmaf(ar[k][s], L2E, h[k][s]) - zhat[s]);  // 0 for non-viable / padding / inactive
+                    es[s] += e[s];
+                }
+                if (tid + k * T < Kc) VS<S>::st(a_xbuf + (uint32_t)((tid + k * T) * S) * 4, e);
+            }
+            int sq = 0;
+            const float r = warp_sum_scatter<S>(es, lane, sq);
+            if ((lane & ((32 / S) - 1)) == 0) sts_v(a_red + (uint32_t)((warp * S + sq) * kCX + 1) * 4, r);
         }
     };
     // α̂/β̂ rows of frame t to HBM — issued after the frame has been shipped, so the
