@@ -625,6 +625,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
     // IZ: log2 Z of the forward, and the normaliser Ẑ of the frame being emitted
     const double logZ2 = IZ ? a.logZ_fwd[b] * 1.4426950408889634 : 0.0;
     float zhat = 0.f;
+    const uint32_t a_cnb = a_cz + 4u * 8u;  // IZ: [2] double, the forward's C of the next two steps' frames
     auto zhat_of = [&](double cn_nat) { return (float)(logZ2 - cn_nat * 1.4426950408889634 - scale); };
     const int dir = BWD ? -1 : 1;
     const int n_first = BWD ? N - 1 : 0;
@@ -757,7 +758,11 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k) { h[k] -= c; uk[k] -= c; }
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n_first] = scale * kLN2;
-        if (IZ) zhat = zhat_of(a.ascale_in[(size_t)b * a.N_max + n_first]);
+        if (IZ) {
+            zhat = zhat_of(a.ascale_in[(size_t)b * a.N_max + n_first]);
+            if (tid == 0)  // C of the first step's frame (step 1) → cnb[1]
+                sts_v(a_cnb + 8u, (double)a.ascale_in[(size_t)b * a.N_max + min(max(n_first + dir, 0), N - 1)]);
+        }
         emit(n_first, h, aA);
         load_v(n_first + 2 * dir, vA);
         if (want_post) load_alpha(n_first + 2 * dir, aA);
@@ -770,9 +775,25 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         __syncthreads();  // u, p, wmax[par], wz[par] of frame n visible
         ++tstep;
         tma_issue(tstep + 1, n_next + dir);  // buffer of step tstep-1 is free now
-        double cn_next = 0.0;  // IZ: the forward's C of frame n_next (used in phase B)
-        if (IZ) cn_next = __ldg(a.ascale_in + (size_t)b * a.N_max + n_next);
-        if (!RAW && warp == 0) {  // the frame's normaliser c and posterior Z, reduced once (read after the next barrier)
+        // IZ: the lagged normaliser c, the float64 offset and Ẑ of frame n_next are formed here,
+        // off phase B's dependency chain (every warp reduces the per-warp maxima itself: an
+        // exact max, the same in every warp)
+        V c_iz = (V)0;
+        if (IZ) {
+            c_iz = block_max_prev(par);
+            if (c_iz == NINF) c_iz = (V)0;
+            scale += (double)c_iz;
+            double cn;  // C of frame n_next: cp.async'd into cnb[tstep & 1] a step ago by thread 0
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cn) : "r"(a_cnb + 8u * (uint32_t)(tstep & 1)));
+            zhat = zhat_of(cn);
+            if (tid == 0) {  // the next step's C (lands during this frame; waited at its end)
+                const int nn = min(max(n_next + dir, 0), N - 1);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(a_cnb + 8u * (uint32_t)((tstep + 1) & 1)),
+                             "l"(a.ascale_in + (size_t)b * a.N_max + nn) : "memory");
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
+        }
+        if (!RAW && !IZ && warp == 0) {  // the frame's normaliser c and posterior Z, reduced once (read after the next barrier)
             const V cmax = block_max_prev(par);
             V Zr = (V)0;
             if (want_post && !IZ) {
@@ -797,11 +818,13 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         if (want_post && !IZ) posterior(n, pp, true);  // γ_n (its x is in registers, Z in cz[pp])
         pend_n = n;
         n = n_next;
-        V c = RAW ? (V)0 : lds_v(a_cz + (uint32_t)(2 * pp) * 8, (V)0);  // lagged normaliser: max of the previous u
-        if (c == NINF) c = (V)0;                // no viable state: keep 0̄ everywhere
-        scale += (double)c;
+        V c = c_iz;
+        if (!IZ) {
+            c = RAW ? (V)0 : lds_v(a_cz + (uint32_t)(2 * pp) * 8, (V)0);  // lagged normaliser: max of the previous u
+            if (c == NINF) c = (V)0;                                       // no viable state: keep 0̄ everywhere
+            scale += (double)c;
+        }
         if (tid == 0 && a.scale) a.scale[(size_t)b * a.N_max + n] = scale * kLN2;
-        if (IZ) zhat = zhat_of(cn_next);
         V h[SPT];
         float vv[SPT];
         fetch_v(tstep, vb, vv);
@@ -828,6 +851,7 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         if (use_mask) states(std::true_type());
         else states(std::false_type());
         emit(n, h, ab);
+        if (IZ && tid == 0) asm volatile("cp.async.wait_all;" ::: "memory");  // next step's C (issued a frame ago)
         load_v(n + 2 * dir, vb);  // refill with the frame two steps ahead
         if (want_post) load_alpha(n + 2 * dir, ab);
         return true;
