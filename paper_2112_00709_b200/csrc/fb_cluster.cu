@@ -384,20 +384,23 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             }
         }
     }
-    float ar[SPT][S];  // α̂ of the frame being produced (backward posteriors), natural log
+    float ar[SPT][S];  // α̂ of the frame being produced (backward posteriors), log2 units
     auto load_alpha = [&](int t) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const bool act = t < Ns[s];
-            if (a.lat_int) {  // internal order: this CTA's part rows are contiguous
-                const float *ro = a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * Kint : 0) + k0 + tid;
+            if (a.lat_int) {  // internal order: this CTA's part rows are contiguous; log2 units
+                const float *ro = a.lat32 ? a.alpha + (act ? ((uint32_t)bs[s] * (uint32_t)N_max + (uint32_t)frame(s, t)) *
+                                                                 (uint32_t)Kint + (uint32_t)(k0 + tid)
+                                                           : (uint32_t)(k0 + tid))
+                                          : a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * Kint : 0) + k0 + tid;
 #pragma unroll
                 for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + k * T) : NEG_INF;
                 continue;
             }
             const float *ro = a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * K : 0);
 #pragma unroll
-            for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + origk[k]) : NEG_INF;
+            for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + origk[k]) * L2E : NEG_INF;
         }
     };
     // x = α̂·log2e + β̂ of the frame whose posterior is pending: xbuf[j][s] (shared memory)
@@ -461,7 +464,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 float x[SPT];
 #pragma unroll
                 for (int k = 0; k < SPT; ++k) {
-                    x[k] = fmaf(ar[k][s], L2E, h[k][s]);
+                    x[k] = ar[k][s] + h[k][s];
                     if (tid + k * T < Kc) sts_v(a_xbuf + (uint32_t)((tid + k * T) * S + s) * 4, x[k]);
                 }
                 float zm, zs;
@@ -497,7 +500,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 float e[S];
 #pragma unroll
                 for (int s = 0; s < S; ++s) {
-                    e[s] = ex2(fmaf(ar[k][s], L2E, h[k][s]) - zhat[s]);  // 0 for non-viable / padding / inactive
+                    e[s] = ex2(ar[k][s] + h[k][s] - zhat[s]);  // 0 for non-viable / padding / inactive
                     es[s] += e[s];
                 }
                 if (tid + k * T < Kc) VS<S>::st(a_xbuf + (uint32_t)((tid + k * T) * S) * 4, e);
@@ -514,11 +517,11 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (t >= Ns[s]) continue;
-            if (a.lat_int) {
+            if (a.lat_int) {  // private lfmmi workspace: internal order, log2 units (no conversion)
                 float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * Kint + k0 + tid;
 #pragma unroll
                 for (int k = 0; k < SPT; ++k)
-                    if (tid + k * T < Kc) latn[k * T] = h[k][s] * LN2;
+                    if (tid + k * T < Kc) latn[k * T] = h[k][s];
                 continue;
             }
             float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * K;
@@ -706,8 +709,15 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     };
     for (int t = 1; t <= Tmax; ++t) {
         const bool last = t == Tmax;
-        if (IZ && tid < S) {  // the forward's C of step t (loaded last frame) → cnbuf; load step t + 1's
-            asm volatile("st.shared.f64 [%0], %1;" ::"r"(a_cn + 8u * (uint32_t)tid), "d"(cn_reg));
+        if (IZ && tid < S) {  // w_s = log2 Z − C_t − D_{t−1} of sequence s = tid → cnbuf (Ẑ_t = w_s − c_t);
+                              // the forward's C of step t was loaded last frame; load step t + 1's
+            double sc = scale[0];
+#pragma unroll
+            for (int q = 1; q < S; ++q) sc = tid == q ? scale[q] : sc;
+            double lz = logZ2[0];
+#pragma unroll
+            for (int q = 1; q < S; ++q) lz = tid == q ? logZ2[q] : lz;
+            sts_v(a_cn + 4u * (uint32_t)tid, (float)(lz - cn_reg * 1.4426950408889634 - sc));
             cn_load(t + 1);
         }
         if (!last) {
@@ -804,9 +814,9 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         const uint32_t eb = a_ebuf + (uint32_t)(t & 1) * EB;
         float c[S];
         int lim[S];
-        // the float64 offsets are needed by every thread only for IZ (Ẑ); otherwise warp 0 of
-        // part 0 keeps them (termination, the scale output) — a CTA-uniform branch
-        const bool keep_scale = IZ || (cr == 0 && warp == 0);
+        // the float64 offsets are kept by warp 0 (IZ: its lanes s < S stage Ẑ's float64 part;
+        // part 0: termination, the scale output) — a CTA-uniform branch
+        const bool keep_scale = warp == 0 && (IZ || cr == 0);
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const bool act = t < Ns[s];
@@ -819,12 +829,11 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 if (t >= Ns[s]) continue;
                 scale[s] += (double)c[s];
                 if (cr == 0 && tid == 0 && a.scale) a.scale[(size_t)bs[s] * N_max + frame(s, t)] = scale[s] * kLN2;
-                if (IZ) {
-                    double cn;
-                    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(cn) : "r"(a_cn + 8u * (uint32_t)s));
-                    zhat[s] = (float)(logZ2[s] - cn * 1.4426950408889634 - scale[s]);
-                }
             }
+        }
+        if (IZ) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) zhat[s] = lds_v(a_cn + 4u * (uint32_t)s, 0.f) - c[s];  // Ẑ_t = w_s − c_t
         }
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {

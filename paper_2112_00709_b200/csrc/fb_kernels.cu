@@ -516,6 +516,7 @@ static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
     const CPlan &P = G.cp;
     FBArgs aa = a;
     aa.tma = (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0);  // 16-byte emission copies
+    aa.lat32 = (size_t)a.B * (size_t)a.N_max * (size_t)P.K_int < ((size_t)1 << 31);
     // the lfmmi den backward normalises γ through the forward's log Z (IZ, fb_cluster.cu)
     const int iz = bwd && a.post_kind == POST_GRAD && a.ascale_in && a.logZ_fwd;
     KFn fn = bwd ? (P.S == 4 ? pick_fbc<true, 4>(P.spt, P.T, P.nop, iz) : pick_fbc<true, 2>(P.spt, P.T, 0, iz))
