@@ -114,6 +114,28 @@ struct VS<4> {
     }
 };
 
+// S-float vectors in global memory (the private α̂ lattice, 8/16-byte aligned)
+template <int S>
+struct VG;
+template <>
+struct VG<2> {
+    static __device__ __forceinline__ void ldg(const float *p, float *v) {
+        const float2 x = __ldg(reinterpret_cast<const float2 *>(p));
+        v[0] = x.x; v[1] = x.y;
+    }
+    static __device__ __forceinline__ void stg(float *p, const float *v) { *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]); }
+};
+template <>
+struct VG<4> {
+    static __device__ __forceinline__ void ldg(const float *p, float *v) {
+        const float4 x = __ldg(reinterpret_cast<const float4 *>(p));
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+    }
+    static __device__ __forceinline__ void stg(float *p, const float *v) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+
 // Phase A over this warp's slices (Sched layout, fb_internal.h) with S-float
 // gathered elements: lane l reduces one row segment for all S sequences.
 // add: accumulate into the part row instead of storing (split schedules).
@@ -282,6 +304,11 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             Tmax = max(Tmax, Ns[s]);
         }
     }
+    // all S sequences of the cluster have one length: the backward reads one frame for all of
+    // them, so the private α̂ lattice is reloaded one vector per state
+    bool eqlen = true;
+#pragma unroll
+    for (int s = 1; s < S; ++s) eqlen = eqlen && Ns[s] == Ns[0];
     // part's pdf range and its emission segment [e_lo, e_lo + e_len)
     const int d_lo = P.pdf_lo[cr], d_hi = P.pdf_lo[cr + 1];
     const bool e16 = a.tma != 0;  // 16-byte emission copies (D % 4 == 0, aligned φ)
@@ -389,13 +416,28 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             const bool act = t < Ns[s];
-            if (a.lat_int) {  // internal order: this CTA's part rows are contiguous; log2 units
-                const float *ro = a.lat32 ? a.alpha + (act ? ((uint32_t)bs[s] * (uint32_t)N_max + (uint32_t)frame(s, t)) *
-                                                                 (uint32_t)Kint + (uint32_t)(k0 + tid)
-                                                           : (uint32_t)(k0 + tid))
-                                          : a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * Kint : 0) + k0 + tid;
+            if (a.lat_int) {  // private layout [cluster][n][K_int][S], log2 units (store_lat)
+                if (eqlen) {   // every sequence of the cluster reads the same frame: one vector per state
+                    if (s == 0) {
+                        const size_t row = ((size_t)grp * N_max + (size_t)(act ? frame(0, t) : 0)) * Kint + k0 + tid;
 #pragma unroll
-                for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + k * T) : NEG_INF;
+                        for (int k = 0; k < SPT; ++k) {
+                            float v[S];
+                            if (act && origk[k] >= 0) {
+                                VG<S>::ldg(a.alpha + (row + (size_t)k * T) * S, v);
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < S; ++q) v[q] = NEG_INF;
+                            }
+#pragma unroll
+                            for (int q = 0; q < S; ++q) ar[k][q] = v[q];
+                        }
+                    }
+                    continue;
+                }
+                const float *ro = a.alpha + (act ? ((size_t)grp * N_max + frame(s, t)) * Kint * S : 0) + (size_t)(k0 + tid) * S + s;
+#pragma unroll
+                for (int k = 0; k < SPT; ++k) ar[k][s] = (act && origk[k] >= 0) ? __ldg(ro + (size_t)k * T * S) : NEG_INF;
                 continue;
             }
             const float *ro = a.alpha + (act ? ((size_t)bs[s] * N_max + frame(s, t)) * K : 0);
@@ -517,11 +559,15 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             if (t >= Ns[s]) continue;
-            if (a.lat_int) {  // private lfmmi workspace: internal order, log2 units (no conversion)
-                float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * Kint + k0 + tid;
+            if (a.lat_int) {  // private lfmmi workspace [cluster][n][K_int][S], log2 units: one vector per state
+                // (frame t = step t for every sequence of the forward; a sequence past its end writes
+                // values no one reads)
+                if (s == 0) {
+                    float *latn = a.lat + (((size_t)grp * N_max + t) * Kint + k0 + tid) * S;
 #pragma unroll
-                for (int k = 0; k < SPT; ++k)
-                    if (tid + k * T < Kc) latn[k * T] = h[k][s];
+                    for (int k = 0; k < SPT; ++k)
+                        if (tid + k * T < Kc) VG<S>::stg(latn + (size_t)k * T * S, h[k]);
+                }
                 continue;
             }
             float *latn = a.lat + ((size_t)bs[s] * N_max + frame(s, t)) * K;

@@ -187,8 +187,7 @@ struct FBArgs {
     int post_kind;
     float *post;        // state / dense pdf / compact pdf / grad (−Γ_den; k_add_num adds Γ_num)
     int tma;            // stage φ rows in shared memory with TMA bulk copies
-    int lat_int;        // cluster kernel: α̂ lattice in the plan's internal state order, rows of K_int
-    int lat32;          // cluster kernel: B·N_max·K_int < 2^31, so lattice offsets fit 32-bit arithmetic
+    int lat_int;        // private lfmmi α̂ lattice: one-CTA kernel rows of K; cluster kernel [cluster][n][K_int][S], log2
                         // (a private lfmmi workspace: coalesced stores and reloads)
     // MODE_RAW (lfmmi numerator): float64 log2 lattices, posteriors normalised by logZ_in
     double *lat64;

@@ -516,7 +516,6 @@ static fb_status launch_fbc(bool bwd, const FBArgs &a, cudaStream_t s) {
     const CPlan &P = G.cp;
     FBArgs aa = a;
     aa.tma = (a.D % 4 == 0) && (((uintptr_t)a.emis & 15) == 0);  // 16-byte emission copies
-    aa.lat32 = (size_t)a.B * (size_t)a.N_max * (size_t)P.K_int < ((size_t)1 << 31);
     // the lfmmi den backward normalises γ through the forward's log Z (IZ, fb_cluster.cu)
     const int iz = bwd && a.post_kind == POST_GRAD && a.ascale_in && a.logZ_fwd;
     KFn fn = bwd ? (P.S == 4 ? pick_fbc<true, 4>(P.spt, P.T, P.nop, iz) : pick_fbc<true, 2>(P.spt, P.T, 0, iz))
@@ -688,7 +687,10 @@ static WsLayout ws_layout(const Graph &num, const Graph &den, int B, int N_max) 
     WsLayout w;
     size_t o = 0;
     // den α̂: rows of K (one CTA per sequence) or of the cluster plan's K_int (internal order)
-    w.den_alpha = o; o += a256((size_t)B * N_max * std::max(den.K_tot, den.cp.ok ? den.cp.K_int : 0) * 4);
+    // den α̂: rows of K (one CTA per sequence) or, for the cluster plan, [cluster][n][K_int][S]
+    // (the S sequences of a cluster interleaved per state: one vector access per state)
+    const size_t Bp = den.cp.ok ? (size_t)((B + den.cp.S - 1) / den.cp.S) * den.cp.S : (size_t)B;
+    w.den_alpha = o; o += a256(Bp * N_max * std::max(den.K_tot, den.cp.ok ? den.cp.K_int : 0) * 4);
     w.num_alpha = o; o += a256((size_t)N_max * num.K_tot * 8);  // float64 when the numerator runs raw
     w.gnum = o; o += a256((size_t)N_max * num.pm.U_tot * 4);
     w.zn = o; o += a256((size_t)B * 8);
