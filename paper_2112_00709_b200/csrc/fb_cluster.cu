@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     const uint32_t a_ebuf = sb + (uint32_t)L.ebuf, a_red = sb + (uint32_t)L.red, a_mbar = sb + (uint32_t)L.mbar;
     const uint32_t a_xbuf = sb + (uint32_t)L.xbuf;
     const uint32_t UB = (uint32_t)fbx_a16(L.ubytes), XOFF = (uint32_t)Kint * S * 4;
-    const uint32_t DC4 = (uint32_t)P.Dc_max * 4;                 // one sequence's emission segment
+    const uint32_t DC4 = (uint32_t)P.Dc_max * 4;                 // one sequence's share of an emission buffer
     const uint32_t EB = (uint32_t)fbx_a16((size_t)S * DC4);      // one emission buffer
     const float L2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
     // u buffer `buf`: rows [Kint][S], then extras slots [C][S][kCX] (max, zm, zs, −)
@@ -311,9 +311,10 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
     for (int s = 1; s < S; ++s) eqlen = eqlen && Ns[s] == Ns[0];
     // part's pdf range and its emission segment [e_lo, e_lo + e_len)
     const int d_lo = P.pdf_lo[cr], d_hi = P.pdf_lo[cr + 1];
-    const bool e16 = a.tma != 0;  // 16-byte emission copies (D % 4 == 0, aligned φ)
-    const int e_lo = e16 ? (d_lo & ~3) : d_lo;
-    const int e_len = (e16 ? min(D, (d_hi + 3) & ~3) : d_hi) - e_lo;
+    // the segment is staged interleaved, [pdf][S]: phase B reads a state's emission for all S
+    // sequences with one vector load (4-byte cp.async per element)
+    const int e_lo = d_lo;
+    const int e_len = d_hi - d_lo;
 
     // ---- padded / skipped frames: −∞ lattice rows, zero posterior rows (own states / own pdf range)
 #pragma unroll
@@ -376,14 +377,10 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             const uint32_t base = a_ebuf + (uint32_t)(t & 1) * EB;
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                if (t >= Ns[s] || (e16 ? 4 * tid : tid) >= e_len) continue;  // only the copying threads
+                if (t >= Ns[s] || tid >= e_len) continue;  // only the copying threads
                 const float *src = a.emis + ((size_t)bs[s] * N_max + frame(s, t)) * D + e_lo;
-                const uint32_t dst = base + (uint32_t)s * DC4;
-                if (e16) {
-                    for (int x = tid; 4 * x < e_len; x += T) cpa16(dst + 16u * (uint32_t)x, src + 4 * x);
-                } else {
-                    for (int x = tid; x < e_len; x += T) cpa4(dst + 4u * (uint32_t)x, src + x);
-                }
+                const uint32_t dst = base + (uint32_t)s * 4u;
+                for (int x = tid; x < e_len; x += T) cpa4(dst + (uint32_t)(x * S) * 4u, src + x);
             }
         }
         cpa_commit();
@@ -398,14 +395,14 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
         const int j = tid + k * T;
-        pdfk[k] = pdf_first * 4;
+        pdfk[k] = pdf_first * S * 4;  // byte offset of the pdf's S-vector in the staged segment
         distk[k] = INT_MAX;
         origk[k] = -1;
         if (j < Kc) {
             const int i = k0 + j;
             origk[k] = P.perm[i];
             if (origk[k] >= 0) {
-                pdfk[k] = (P.ipdf[i] - e_lo) * 4;
+                pdfk[k] = (P.ipdf[i] - e_lo) * S * 4;
                 distk[k] = BWD ? P.idist_start[i] : P.idist_fin[i];
                 if (!(BWD ? G.mask_bwd : G.mask_fwd)) distk[k] = 0;
             }
@@ -662,7 +659,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
             for (int k = 0; k < SPT; ++k) {
                 const int j = tid + k * T;
                 const bool ok = distk[k] <= lim;
-                const float v = lds_v(a_ebuf + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
+                const float v = lds_v(a_ebuf + (uint32_t)pdfk[k] + 4u * (uint32_t)s, 0.f);
                 if (act) vsum[s] += v;
                 const float v2 = v * L2E;
                 const int jj = min(j, Kc - 1);
@@ -891,9 +888,11 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 VS<S>::st(a_part + (uint32_t)(j * S) * 4, z);
             }
             float alo = 1.f, ahi = 1.f;  // range of the viable sums (the fallback test, once per state)
+            float ev[S];
+            VS<S>::ld(eb + (uint32_t)pdfk[k], ev);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                const float v = lds_v(eb + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
+                const float v = ev[s];
                 vsum[s] += lim[s] >= 0 ? v : 0.f;  // inactive sequences' buffers are stale
                 const bool ok = distk[k] <= lim[s];
                 const float am = ok ? acc[s] : 1.f;
@@ -914,7 +913,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                     if (!(distk[k] <= lim[s]) || (acc[s] >= kTiny && acc[s] <= kHuge)) continue;
                     const float y = exact_row_c<S, NOP>(BWD ? P.bptr : P.fptr, BWD ? P.bsrc : P.fsrc, BWD ? P.bw2 : P.fw2,
                                                    k0 + j, s, up, G.ctr + 1);
-                    const float v = lds_v(eb + (uint32_t)s * DC4 + (uint32_t)pdfk[k], 0.f);
+                    const float v = lds_v(eb + (uint32_t)pdfk[k] + 4u * (uint32_t)s, 0.f);
                     if (!BWD) {
                         h[k][s] = y + fmaf(v, L2E, -c[s]);
                         u[k][s] = h[k][s];
