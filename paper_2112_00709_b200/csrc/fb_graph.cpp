@@ -370,8 +370,10 @@ bool build_cluster_plan(const RowLists &in, const RowLists &out, int K, int D, c
     // no-p (4,4) paper-shape plan (N2 fwd 5.36 → 5.12 ms, bwd 8.72 → 8.36 ms), slower
     // for (2,2) on C3/C4 (6.52 → 6.94 ms); FBX_CLUSTER_SPLIT=0|1 overrides
     // bit 0: forward, bit 1: backward.  With p-exchange (round 2) the forward is faster
-    // unsplit (N2 3.72 → 3.60 ms) while the backward keeps the split (5.73 vs 5.77 ms).
-    cp.split = nop ? 2 : 0;
+    // unsplit (N2 3.72 → 3.60 ms); after the lighter phase B of the IZ epilogue, interleaved
+    // emissions and vector lattice accesses the backward is too (N2 bwd 4.27 → 4.19 ms, step
+    // 7.57 → 7.49 ms), so no plan splits by default.
+    cp.split = 0;
     if (const char *e = std::getenv("FBX_CLUSTER_SPLIT"))  // 0 none, 1 both, f forward only, b backward only
         cp.split = e[0] == 'f' ? 1 : e[0] == 'b' ? 2 : (std::atoi(e) != 0 ? 3 : 0);
     std::vector<double> cost(D, 0.0);

@@ -328,14 +328,14 @@ def test_viterbi_paper_shape_n2(fbx):
 
 # ------------------------------------------------------------------ cluster-batched kernel (k_fbc)
 
-@pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2", "4,4,1", "4,4,1/split0", "4,4,1/splitf", "2,2/split1",
-                                "8,4/split1", "8,4,1"])
+@pytest.mark.parametrize("cs", ["2,2", "4,2", "2,4", "4,4", "8,2", "4,4,1", "4,4,1/split1", "4,4,1/splitf",
+                                "4,4,1/splitb", "2,2/split1", "8,4/split1", "8,4,1"])
 def test_cluster_configs_vs_oracle(fbx, cs, monkeypatch):
     """Every (C CTAs, S sequences) cluster configuration of a shared factored
     graph against the oracle: logZ (both directions), α̂ + scale, state and pdf
     posteriors, ragged lengths (a length-1 sequence, an odd batch).  /splitX
-    forces phase A's local/remote arc split (0 none, 1 both directions, f forward only; default: backward
-    only for no-p plans)."""
+    forces phase A's local/remote arc split (0 none, 1 both directions, f forward only, b backward
+    only; default: none)."""
     if "/split" in cs:
         cs, sp = cs.split("/split")
         monkeypatch.setenv("FBX_CLUSTER_SPLIT", sp)
