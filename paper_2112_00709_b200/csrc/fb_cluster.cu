@@ -385,6 +385,10 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
         }
         cpa_commit();
     };
+    // both emission buffers start at 0: a sequence past its end (or a padding sequence) then
+    // reads finite values it has read before (or 0), so vsum needs no per-element guard
+    for (int x = tid; 4 * x < 2 * (int)EB; x += T) sts_v(a_ebuf + 4u * (uint32_t)x, 0.f);
+    __syncthreads();
     emis_issue(0);
     emis_issue(1);
 
@@ -809,7 +813,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
                 }
             }
             // IZ: Z[s] carries the pdf-row multiplier −1/S (0 if S is not a positive finite sum)
-            const float zl = IZ ? ((zm > 0.f && zm < INFINITY) ? -1.f / zm : 0.f)
+            const float zl = IZ ? ((zm > 0.f && zm < INFINITY) ? -__fdividef(1.f, zm) : 0.f)
                                 : ((zm == NEG_INF) ? NEG_INF : zm + lg2(zs));
 #pragma unroll
             for (int s = 0; s < S; ++s) {
@@ -893,7 +897,7 @@ __global__ void __launch_bounds__(T, 1) k_fbc(const FBArgs a) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const float v = ev[s];
-                vsum[s] += lim[s] >= 0 ? v : 0.f;  // inactive sequences' buffers are stale
+                vsum[s] += v;  // inactive sequences read stale finite values or 0 (zeroed buffers)
                 const bool ok = distk[k] <= lim[s];
                 const float am = ok ? acc[s] : 1.f;
                 alo = fminf(alo, am);
