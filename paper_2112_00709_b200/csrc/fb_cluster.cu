@@ -153,7 +153,7 @@ __device__ __forceinline__ void phase_a_vec(uint32_t cur, int nsl, int lane, uin
         float2 a0[S / 2], a1[S / 2];
 #pragma unroll
         for (int i = 0; i < S / 2; ++i) { a0[i] = make_float2(0.f, 0.f); a1[i] = make_float2(0.f, 0.f); }
-#pragma unroll 2
+#pragma unroll 4
         for (int s = 0; s < L2; ++s) {
             const uint32_t ix = lds_u32(ia);
             const float2 w2 = lds_f2(wa);
