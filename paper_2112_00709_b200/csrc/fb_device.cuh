@@ -406,6 +406,25 @@ __device__ __forceinline__ void pdf_row(const FBArgs &a, uint32_t a_gbuf, uint32
     }
 }
 
+// The gradient row of the IZ backward when no pdf has more than two states: pq[d] holds two
+// byte offsets into the γ buffer (a state's e, or a zero cell), so a pdf costs two loads and
+// an add — no count decode, no branches.
+__device__ __forceinline__ void pdf_row_pair2(const FBArgs &a, uint32_t a_gbuf, uint32_t a_pq, int b, int n, int tid,
+                                              int T, float mul) {
+    const int D = a.D;
+    float *row = a.post + ((size_t)b * a.N_max + n) * D;
+    auto run = [&](uint32_t w) { return mul * (lds_v(a_gbuf + (w & 0xFFFFu), 0.f) + lds_v(a_gbuf + (w >> 16), 0.f)); };
+    if ((D & 1) == 0 && ((uintptr_t)a.post & 7) == 0) {
+        for (int i = tid; 2 * i < D; i += T) {
+            uint32_t w0, w1;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "r"(a_pq + 8 * (uint32_t)i));
+            *reinterpret_cast<float2 *>(row + 2 * i) = make_float2(run(w0), run(w1));
+        }
+    } else {
+        for (int d = tid; d < D; d += T) row[d] = run(lds_u32(a_pq + 4 * (uint32_t)d));
+    }
+}
+
 // Zero (posterior) / −∞ (lattice) rows for frames [n0, n1).
 inline __device__ void write_pad_rows(const FBArgs &a, int gi, int b, int K, int s0, int n0, int n1, int tid, int T,
                                bool lattice, bool bwd) {
@@ -515,6 +534,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         for (int x = tid; x < n16; x += T) dst[x] = src[x];
     }
     if (tid == 0) sts_i(a_flag, 0);
+    // IZ gradient rows with ≤ 2 states per pdf and a spare γ slot: the two-offset pq form
+    const bool pair2 = IZ && G.pm.spp_max <= 2 && K < T * SPT && T * SPT * 4 <= 65536;
     // pdf-level epilogue maps → shared memory
     if (pdf_post) {
         const int so = G.pm.slot_off[gi], U = G.pm.slot_off[gi + 1] - so;
@@ -526,8 +547,14 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
                 const int sl = G.pm.pdf_slot[(size_t)gi * a.D + d];
                 const int q0 = sl < 0 ? 0 : G.pm.slot_sptr[so + sl] - base;
                 const int c = sl < 0 ? 0 : G.pm.slot_sptr[so + sl + 1] - G.pm.slot_sptr[so + sl];
-                pq[d] = (uint32_t)q0 | ((uint32_t)c << 16);
+                if (pair2) {  // byte offsets of the pdf's (up to) two states, else of the zero cell
+                    const uint32_t z = (uint32_t)(T * SPT - 1) * 4u;
+                    pq[d] = (c >= 1 ? (uint32_t)q0 * 4u : z) | ((c >= 2 ? (uint32_t)(q0 + 1) * 4u : z) << 16);
+                } else {
+                    pq[d] = (uint32_t)q0 | ((uint32_t)c << 16);
+                }
             }
+        if (pair2 && tid == 0) sts_v(a_gbuf + (uint32_t)(T * SPT - 1) * 4u, 0.f);  // the zero cell (never a state's)
     }
     const int nsl = S.warp_nsl[gi * W + warp];
     const int nsl0 = S.warp_nsl0[gi * W + warp];
@@ -718,7 +745,8 @@ __device__ __forceinline__ void fb_sequence(const FBArgs &a, const int b) {
         float sv = lane < W ? lds_v(a_wz + (uint32_t)(pp * 64 + lane) * 8, 0.f) : 0.f;
         sv = warp_sum(sv);  // every warp the same S (same partials, same order)
         const float mul = (sv > 0.f && sv < INFINITY) ? -__fdividef(1.f, sv) : 0.f;
-        pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pn, tid, T, mul);
+        if (pair2) pdf_row_pair2(a, a_gbuf, a_pq, b, pn, tid, T, mul);
+        else pdf_row(a, a_gbuf, a_ssp, a_pq, gi, b, pn, tid, T, mul);
     };
     auto block_max_prev = [&](int pp) {
         const V v = lane < W ? lds_v(a_wmax + (uint32_t)(pp * 32 + lane) * 8, (V)0) : NINF;

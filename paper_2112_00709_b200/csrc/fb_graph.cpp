@@ -920,6 +920,8 @@ static fb_status create_impl(fb_graph *out, int32_t G, const int32_t *state_offs
         slot_sptr.push_back((int)slot_states.size());
         slot_off[g + 1] = slot_off[g] + local;
         gr.pm.U_max = std::max(gr.pm.U_max, local);
+        for (int x = slot_off[g]; x < slot_off[g + 1]; ++x)
+            gr.pm.spp_max = std::max(gr.pm.spp_max, slot_sptr[x + 1] - slot_sptr[x]);
         // literal batch matrix rows: in-arcs of every state, then the phony state's row
         lit_row_off[g] = (int)lit_ptr.size() - 1;
         for (int j = 0; j < K; ++j) {

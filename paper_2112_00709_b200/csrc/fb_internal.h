@@ -60,6 +60,7 @@ struct PdfMap {
     const int *slot_pos = nullptr;    // [K_tot] position of a state in its member's slot-ordered list
     int U_max = 0;
     long long U_tot = 0;
+    int spp_max = 0;                  // most states sharing one pdf in a member
 };
 
 // Cluster plan of a shared (G == 1) factored graph for k_fbc: a thread-block
